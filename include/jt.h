@@ -1,0 +1,136 @@
+/* jt.h — C ABI of the B200-native fast Jacobi polynomial transform library (libjt.so).
+ *
+ * Implements the hot path of arXiv 1901.07275 (Bremer, Pang, Yang), "Fast Algorithms for the
+ * Multi-dimensional Jacobi Polynomial Transform":  the d-dimensional (d = 1, 2, 3) UNIFORM forward
+ * and inverse discrete Jacobi transform, applied in the factored form
+ *
+ *     W J_n = [ W V_n , W Re( B_n (.) F_n ) ],   B_n ~ sum_{l<r} u_l v_l^T     (PAPER.md:576-615,
+ *                                                   eq:B, eq:lastJ, eq:permuDFT, eq:approxA, eq:oneJ)
+ *
+ * axis by axis (eq:TJ PAPER.md:669-674, eq:TJ3 PAPER.md:718-722), each axis pass a hand-written
+ * sm_100a CUDA kernel (fp64 FFTs, no cuFFT).  Plans are built on the host (Gauss-Jacobi rule,
+ * non-oscillatory P~ + iQ~ = M e^{i psi}; Algorithm 1).
+ *
+ * Conventions (all calls):
+ *   - Arrays are fp64, C-order (row-major), shape n[0] x ... x n[d-1]; axis i uses (a[i], b[i]).
+ *   - Coefficient index along an axis = polynomial degree k (0-based, PAPER.md:485 tf:transexp).
+ *   - Value index along an axis = quadrature node j, nodes t_j ascending in (0, pi).
+ *   - jt_forward computes values = (Phi_0 (x) ... (x) Phi_{d-1}) coeffs with the orthogonal
+ *     Phi_i = W_i J_i, Phi_i[j,k] = sqrt(w_j) P~_k(t_j)  (PAPER.md:460-470 tf:transout, 495-509,
+ *     663, 706).  These are the paper's WEIGHTED values W f; unweighted f_j = values_j / sqrt(w_j).
+ *   - jt_inverse computes coeffs = (Phi_0^T (x) ... (x) Phi_{d-1}^T) values (the uniform inverse,
+ *     eq:oneJinv PAPER.md:621-630, eq:invTJ PAPER.md:683-687, eq:invTJ3 PAPER.md:731-735).
+ *   - Every call returns a jt_status; no C++ exception crosses the ABI.  On a non-OK status,
+ *     jt_last_error() returns a thread-local human-readable message.
+ *   - Device-pointer calls enqueue work on `cuda_stream` (a cudaStream_t; NULL = legacy default
+ *     stream) and return without synchronising.  One in-flight call per plan at a time.
+ */
+#ifndef JT_H
+#define JT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct jt_plan_s *jt_plan_t; /* opaque plan handle */
+
+typedef enum {
+  JT_OK = 0,
+  JT_ERR_ARG = 1,     /* bad argument: d not in {1,2,3}, n[i] < 2 or > 4096, eps not in [1e-15, 1e-2],
+                         null pointer, aliasing in/out where not allowed, host-only plan on a device call */
+  JT_ERR_DOMAIN = 2,  /* a or b outside (-1, 1): the paper's validated range, "not applicable" outside
+                          */
+  JT_ERR_NUMERIC = 3, /* Newton for the nodes did not converge, or the adaptive rank exceeded its cap */
+  JT_ERR_ALLOC = 4,   /* host or device allocation failed */
+  JT_ERR_CUDA = 5,    /* a CUDA runtime error (launch, copy, or an asynchronous fault from an earlier call) */
+  JT_ERR_NCCL = 6     /* reserved for the library-owned NCCL path */
+} jt_status;
+
+/* Plan options.  jt_default_opts() fills the defaults shown. */
+typedef struct {
+  uint64_t seed;   /* PRNG seed of Algorithm 1's random row/column samples (default 0) */
+  int k0;          /* number of low degrees kept in the dense block V (default 27) */
+  int rmax_init;   /* initial rank cap of Algorithm 1; 0 = max(ceil(2 log2 n), 32) */
+  int q;           /* oversampling factor of Algorithm 1 (default 3; "q = O(1)") */
+  int sweeps;      /* repetitions of Algorithm 1 steps 2-3 (default 2) */
+  int device;      /* CUDA device ordinal for the plan's buffers; -1 = current device;
+                      -2 = HOST-ONLY plan (no GPU touched: introspection only, device calls fail) */
+} jt_opts;
+
+/* Fill *o with the defaults above.  Returns JT_ERR_ARG if o is NULL. */
+jt_status jt_default_opts(jt_opts *o);
+
+/* Build a plan for a d-dimensional uniform transform (d in {1,2,3}).
+ *   n[i]   length of axis i, 2 <= n[i] <= 4096;
+ *   a[i], b[i]  Jacobi parameters of axis i, in (-1, 1);
+ *   eps    relative tolerance of the low-rank factorisation of B (truncation sigma_{r+1} <= eps sigma_1,
+ *          PAPER.md:238), in [1e-15, 1e-2];
+ *   opts   NULL for defaults.
+ * Host work per axis: O(n^2) long-double recurrences (nodes, P~ + iQ~), Algorithm 1 in O(n r^2 q);
+ * then one host->device upload of the factors (unless opts->device == -2).
+ * On success *out owns all host and device buffers of the plan; free it with jt_destroy. */
+jt_status jt_plan(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
+                  double eps, const jt_opts *opts);
+
+/* Forward transform, device pointers (fp64, C-order, prod(n) elements each, 16-byte aligned).
+ * coeffs is read-only; values is written.  coeffs == values is allowed (in place); partial overlap
+ * is JT_ERR_ARG.  Runs d fused axis passes. */
+jt_status jt_forward(jt_plan_t p, const double *coeffs, double *values, void *cuda_stream);
+
+/* Inverse (transpose) transform, device pointers; same layout/aliasing rules as jt_forward. */
+jt_status jt_inverse(jt_plan_t p, const double *values, double *coeffs, void *cuda_stream);
+
+/* End-to-end variants with HOST buffers (pageable or pinned): copies host->device, transforms,
+ * copies device->host, then synchronises `cuda_stream`.  Uses plan-owned device staging buffers. */
+jt_status jt_forward_host(jt_plan_t p, const double *coeffs_host, double *values_host, void *cuda_stream);
+jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs_host, void *cuda_stream);
+
+/* One axis pass (the building block of the slab-distributed schedule):
+ * applies axis `axis`'s 1D forward (inverse) transform along the middle index of an
+ * (outer, n[axis], inner) C-order device array.  in == out allowed (in place). */
+jt_status jt_forward_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer,
+                          int64_t inner, void *cuda_stream);
+jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer,
+                          int64_t inner, void *cuda_stream);
+
+/* Free a plan (device buffers included).  jt_destroy(NULL) is JT_OK. */
+jt_status jt_destroy(jt_plan_t p);
+
+/* ---- introspection (host; valid for host-only plans too) ---- */
+
+/* Rank r of axis `axis`'s factorisation (number of FFT terms per line). */
+jt_status jt_plan_rank(jt_plan_t p, int axis, int *r);
+
+/* Per-axis sizes: n, the FFT length N (power of two >= max(n,16)), effective k0 = min(k0, n), r. */
+jt_status jt_plan_info(jt_plan_t p, int axis, int64_t *n, int64_t *nfft, int *k0, int *r);
+
+/* Nodes t_j (ascending, (0, pi)) and trigonometric weights w_j of axis `axis` into host arrays of
+ * length n (introduction:modrule; reading R2 of DESIGN.md).  Either may be NULL. */
+jt_status jt_plan_nodes(jt_plan_t p, int axis, double *t_host, double *w_host);
+
+/* Factors of axis `axis` into host arrays (any may be NULL):
+ *   u_host    n x r complex (interleaved re,im), column l = u~_l = W u_l S^{1/2} (weights folded)
+ *   v_host    r x N complex (interleaved), row l = v_l; zero for k < k0 and k >= n
+ *   phiv_host n x k0 real, Phi_V[j,k] = sqrt(w_j) P~_k(t_j), k < k0 (the block W V)
+ *   bins_host n int32, m_j = nearest integer to t_j N / (2 pi) (ties to even).
+ * So that Phi[j,k] ~ phiv[j,k] (k<k0), Re(sum_l u[j,l] v[l,k] e^{2 pi i m_j k / N}) (k>=k0). */
+jt_status jt_plan_factors(jt_plan_t p, int axis, double *u_host, double *v_host, double *phiv_host,
+                          int32_t *bins_host);
+
+/* Diagnostics of axis `axis`'s factorisation: the singular values sigma_0..sigma_{count-1} of
+ * Algorithm 1's middle matrix (descending; count <= rmax; pass sigma=NULL to query count) and the
+ * rank cap used. */
+jt_status jt_plan_sigma(jt_plan_t p, int axis, double *sigma, int *count, int *rmax_used);
+
+/* Thread-local text of the last non-OK status ("" if none). */
+const char *jt_last_error(void);
+
+/* Library version string. */
+const char *jt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JT_H */

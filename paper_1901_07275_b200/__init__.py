@@ -1,0 +1,278 @@
+"""B200-native fast multi-dimensional Jacobi polynomial transform (arXiv 1901.07275).
+
+Thin ctypes binding over the C ABI of `libjt.so` (include/jt.h): argument marshalling only; every
+step of the transform runs in the library's sm_100a kernels, every step of the plan in its host C++.
+PyTorch supplies device memory and streams (tensors are passed by `data_ptr()`).
+
+There is no CPU fallback: importing this package fails loudly if `libjt.so` has not been built
+(`python -m paper_1901_07275_b200.build`), and device calls fail with a JTError if no GPU is present.
+
+Names follow the C ABI: jt_plan / jt_forward / jt_inverse / jt_destroy (+ introspection), plus a
+convenience `Plan` class.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libjt.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1901_07275_b200.build` "
+                      "(there is deliberately no fallback path)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+JT_OK, JT_ERR_ARG, JT_ERR_DOMAIN, JT_ERR_NUMERIC, JT_ERR_ALLOC, JT_ERR_CUDA, JT_ERR_NCCL = range(7)
+_STATUS = {0: "JT_OK", 1: "JT_ERR_ARG", 2: "JT_ERR_DOMAIN", 3: "JT_ERR_NUMERIC", 4: "JT_ERR_ALLOC",
+           5: "JT_ERR_CUDA", 6: "JT_ERR_NCCL"}
+
+# Every symbol declared in include/jt.h and include/jt_debug.h (checked by tests/test_abi.py).
+EXPORTED = ["jt_default_opts", "jt_plan", "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
+            "jt_forward_axis", "jt_inverse_axis", "jt_destroy", "jt_plan_rank", "jt_plan_info",
+            "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_error", "jt_version",
+            "jt_debug_modified_pq"]
+
+
+class JTError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.jt_last_error().decode()
+        super().__init__(f"{where}: {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class jt_opts(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("k0", ctypes.c_int), ("rmax_init", ctypes.c_int),
+                ("q", ctypes.c_int), ("sweeps", ctypes.c_int), ("device", ctypes.c_int)]
+
+
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.POINTER(ctypes.c_int64)
+_lib.jt_default_opts.argtypes = [ctypes.POINTER(jt_opts)]
+_lib.jt_plan.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double, ctypes.POINTER(jt_opts)]
+for _f in ("jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host"):
+    getattr(_lib, _f).argtypes = [_P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+for _f in ("jt_forward_axis", "jt_inverse_axis"):
+    getattr(_lib, _f).argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                  ctypes.c_int64, ctypes.c_void_p]
+_lib.jt_destroy.argtypes = [_P]
+_lib.jt_plan_rank.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+_lib.jt_plan_info.argtypes = [_P, ctypes.c_int, _I64, _I64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+_lib.jt_plan_nodes.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+_lib.jt_plan_factors.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.jt_plan_sigma.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
+                               ctypes.POINTER(ctypes.c_int)]
+_lib.jt_last_error.restype = ctypes.c_char_p
+_lib.jt_version.restype = ctypes.c_char_p
+_lib.jt_debug_modified_pq.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p,
+                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+for _f in EXPORTED:
+    if _f not in ("jt_last_error", "jt_version"):
+        getattr(_lib, _f).restype = ctypes.c_int
+
+
+def _check(status: int, where: str):
+    if status != JT_OK:
+        raise JTError(status, where)
+
+
+def _ptr(x) -> int:
+    """Device or host address of a torch tensor / numpy array (C-contiguous float64 required)."""
+    if isinstance(x, np.ndarray):
+        if x.dtype != np.float64 or not x.flags.c_contiguous:
+            raise ValueError("numpy arrays must be C-contiguous float64")
+        return x.ctypes.data
+    if x.dtype.__repr__() != "torch.float64" or not x.is_contiguous():
+        raise ValueError("tensors must be contiguous torch.float64")
+    return x.data_ptr()
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def jt_version() -> str:
+    return _lib.jt_version().decode()
+
+
+def jt_default_opts() -> jt_opts:
+    o = jt_opts()
+    _check(_lib.jt_default_opts(ctypes.byref(o)), "jt_default_opts")
+    return o
+
+
+def jt_plan(n, a, b, eps: float = 1e-12, seed: int = 0, k0: int = 27, rmax_init: int = 0, q: int = 3,
+            sweeps: int = 2, device: int = -1) -> int:
+    """Build a plan (C: jt_plan).  device=-1: current CUDA device; device=-2: host-only plan."""
+    n = [int(v) for v in np.atleast_1d(n)]
+    d = len(n)
+    a = np.broadcast_to(np.asarray(a, dtype=np.float64), (d,)).copy()
+    b = np.broadcast_to(np.asarray(b, dtype=np.float64), (d,)).copy()
+    o = jt_default_opts()
+    o.seed, o.k0, o.rmax_init, o.q, o.sweeps, o.device = seed, k0, rmax_init, q, sweeps, device
+    h = _P()
+    _check(_lib.jt_plan(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D), b.ctypes.data_as(_D),
+                        float(eps), ctypes.byref(o)), "jt_plan")
+    return h.value
+
+
+def jt_forward(plan: int, coeffs, values, stream=None):
+    _check(_lib.jt_forward(plan, _ptr(coeffs), _ptr(values), _stream_handle(stream)), "jt_forward")
+
+
+def jt_inverse(plan: int, values, coeffs, stream=None):
+    _check(_lib.jt_inverse(plan, _ptr(values), _ptr(coeffs), _stream_handle(stream)), "jt_inverse")
+
+
+def jt_forward_host(plan: int, coeffs_host: np.ndarray, values_host: np.ndarray, stream=None):
+    _check(_lib.jt_forward_host(plan, _ptr(coeffs_host), _ptr(values_host), _stream_handle(stream)),
+           "jt_forward_host")
+
+
+def jt_inverse_host(plan: int, values_host: np.ndarray, coeffs_host: np.ndarray, stream=None):
+    _check(_lib.jt_inverse_host(plan, _ptr(values_host), _ptr(coeffs_host), _stream_handle(stream)),
+           "jt_inverse_host")
+
+
+def jt_forward_axis(plan: int, axis: int, x_in, x_out, outer: int, inner: int, stream=None):
+    _check(_lib.jt_forward_axis(plan, axis, _ptr(x_in), _ptr(x_out), outer, inner, _stream_handle(stream)),
+           "jt_forward_axis")
+
+
+def jt_inverse_axis(plan: int, axis: int, x_in, x_out, outer: int, inner: int, stream=None):
+    _check(_lib.jt_inverse_axis(plan, axis, _ptr(x_in), _ptr(x_out), outer, inner, _stream_handle(stream)),
+           "jt_inverse_axis")
+
+
+def jt_destroy(plan: int):
+    _check(_lib.jt_destroy(plan), "jt_destroy")
+
+
+def jt_plan_rank(plan: int, axis: int) -> int:
+    r = ctypes.c_int()
+    _check(_lib.jt_plan_rank(plan, axis, ctypes.byref(r)), "jt_plan_rank")
+    return r.value
+
+
+def jt_plan_info(plan: int, axis: int) -> dict:
+    n, N, k0, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int()
+    _check(_lib.jt_plan_info(plan, axis, ctypes.byref(n), ctypes.byref(N), ctypes.byref(k0), ctypes.byref(r)),
+           "jt_plan_info")
+    return {"n": n.value, "N": N.value, "k0": k0.value, "r": r.value}
+
+
+def jt_plan_nodes(plan: int, axis: int):
+    n = jt_plan_info(plan, axis)["n"]
+    t = np.empty(n)
+    w = np.empty(n)
+    _check(_lib.jt_plan_nodes(plan, axis, t.ctypes.data, w.ctypes.data), "jt_plan_nodes")
+    return t, w
+
+
+def jt_plan_factors(plan: int, axis: int):
+    """(u (n x r complex), v (r x N complex), phiv (n x k0), bins (n int32)) — see include/jt.h."""
+    info = jt_plan_info(plan, axis)
+    n, N, k0, r = info["n"], info["N"], info["k0"], info["r"]
+    u = np.zeros((n, r), dtype=np.complex128)
+    v = np.zeros((r, N), dtype=np.complex128)
+    phiv = np.zeros((n, k0), dtype=np.float64)
+    bins = np.zeros(n, dtype=np.int32)
+    _check(_lib.jt_plan_factors(plan, axis, u.ctypes.data, v.ctypes.data, phiv.ctypes.data, bins.ctypes.data),
+           "jt_plan_factors")
+    return u, v, phiv, bins
+
+
+def jt_plan_sigma(plan: int, axis: int):
+    cnt, rmax = ctypes.c_int(), ctypes.c_int()
+    _check(_lib.jt_plan_sigma(plan, axis, None, ctypes.byref(cnt), ctypes.byref(rmax)), "jt_plan_sigma")
+    s = np.zeros(cnt.value)
+    _check(_lib.jt_plan_sigma(plan, axis, s.ctypes.data, ctypes.byref(cnt), ctypes.byref(rmax)), "jt_plan_sigma")
+    return s, rmax.value
+
+
+def jt_debug_modified_pq(a: float, b: float, t, kmax: int):
+    """P~_k(t), Q~_k(t) for k = 0..kmax by the plan's route (include/jt_debug.h)."""
+    t = np.ascontiguousarray(np.atleast_1d(t), dtype=np.float64)
+    P = np.zeros((t.size, kmax + 1))
+    Q = np.zeros((t.size, kmax + 1))
+    _check(_lib.jt_debug_modified_pq(a, b, t.size, t.ctypes.data, kmax, P.ctypes.data, Q.ctypes.data),
+           "jt_debug_modified_pq")
+    return P, Q
+
+
+class Plan:
+    """Owning wrapper: Plan(n, a, b, eps) -> .forward(x) / .inverse(y) on CUDA float64 tensors."""
+
+    def __init__(self, n, a, b, eps: float = 1e-12, **kw):
+        self.shape = tuple(int(v) for v in np.atleast_1d(n))
+        self.d = len(self.shape)
+        self.handle = jt_plan(self.shape, a, b, eps, **kw)
+
+    def _out(self, x, out):
+        if out is None:
+            import torch
+            out = torch.empty(self.shape, dtype=torch.float64, device=x.device)
+        if tuple(x.shape) != self.shape or tuple(out.shape) != self.shape:
+            raise ValueError(f"expected shape {self.shape}")
+        return out
+
+    def forward(self, coeffs, out=None, stream=None):
+        out = self._out(coeffs, out)
+        jt_forward(self.handle, coeffs, out, stream)
+        return out
+
+    def inverse(self, values, out=None, stream=None):
+        out = self._out(values, out)
+        jt_inverse(self.handle, values, out, stream)
+        return out
+
+    def forward_host(self, coeffs: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.empty(self.shape) if out is None else out
+        jt_forward_host(self.handle, coeffs, out, stream)
+        return out
+
+    def inverse_host(self, values: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        out = np.empty(self.shape) if out is None else out
+        jt_inverse_host(self.handle, values, out, stream)
+        return out
+
+    def rank(self, axis: int = 0) -> int:
+        return jt_plan_rank(self.handle, axis)
+
+    def info(self, axis: int = 0) -> dict:
+        return jt_plan_info(self.handle, axis)
+
+    def nodes(self, axis: int = 0):
+        return jt_plan_nodes(self.handle, axis)
+
+    def factors(self, axis: int = 0):
+        return jt_plan_factors(self.handle, axis)
+
+    def sigma(self, axis: int = 0):
+        return jt_plan_sigma(self.handle, axis)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            jt_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

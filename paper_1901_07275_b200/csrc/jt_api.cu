@@ -1,0 +1,429 @@
+// C ABI of libjt.so (include/jt.h): plan lifetime, host->device upload of the per-axis factors,
+// and the axis-pass schedule of the d-dimensional transform (eq:TJ PAPER.md:669-674, eq:TJ3
+// PAPER.md:718-722): one fused kernel launch per axis, the first reading the input array, the rest in
+// place on the output array.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "fused_axis.cuh"
+#include "jt_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+jt_status fail(jt_status s, const std::string &msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define JT_CUDA_TRY(expr)                                                                      \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) return fail(JT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct AxisDevBuf {
+  double2 *u = nullptr, *v = nullptr, *tw = nullptr;
+  double *phiv = nullptr;
+  int *bstart = nullptr;
+};
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      changed = cudaSetDevice(dev) == cudaSuccess;
+    }
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct jt_plan_s {
+  int d = 0;
+  int64_t n[3] = {0, 0, 0};
+  double a[3] = {0, 0, 0}, b[3] = {0, 0, 0}, eps = 0;
+  jt_opts opts{};
+  int device = -2;  // -2: host-only
+  jt::AxisHost host[3];
+  AxisDevBuf dev[3];
+  int64_t total = 0;
+  double *stage_in = nullptr, *stage_out = nullptr;  // for the *_host entry points
+};
+
+namespace {
+
+jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
+  const jt::AxisHost &h = p->host[axis];
+  jtk::AxisDev ax;
+  ax.n = (int)h.n;
+  ax.N = (int)h.N;
+  ax.k0 = h.k0;
+  ax.r = h.r;
+  ax.u = p->dev[axis].u;
+  ax.v = p->dev[axis].v;
+  ax.phiv = p->dev[axis].phiv;
+  ax.bstart = p->dev[axis].bstart;
+  ax.tw = p->dev[axis].tw;
+  return ax;
+}
+
+template <int N>
+constexpr int lines_for() {
+  return N <= 128 ? 32 : (N == 256 ? 16 : (N == 512 ? 8 : (N == 1024 ? 4 : (N == 2048 ? 2 : 1))));
+}
+
+template <int N>
+jt_status launch_n(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
+                   long long inner, cudaStream_t s) {
+  constexpr int R = 16;
+  constexpr int LINES = lines_for<N>();
+  using G = jtk::Geo<N, R, LINES>;
+  const size_t smem = G::smem_bytes(ax.k0);
+  const long long blocks = (nlines + LINES - 1) / LINES;
+  if (blocks == 0) return JT_OK;
+  if (inverse) {
+    auto kern = jtk::inv_axis_kernel<N, R, LINES>;
+    JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)blocks, G::NT, smem, s>>>(ax, in, out, nlines, inner);
+  } else {
+    auto kern = jtk::fwd_axis_kernel<N, R, LINES>;
+    JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)blocks, G::NT, smem, s>>>(ax, in, out, nlines, inner);
+  }
+  JT_CUDA_TRY(cudaGetLastError());
+  return JT_OK;
+}
+
+jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
+                      long long inner, cudaStream_t s) {
+  jtk::AxisDev ax = axis_dev(p, axis);
+  const long long nlines = outer * inner;
+  switch (ax.N) {
+    case 16: return launch_n<16>(inverse, ax, in, out, nlines, inner, s);
+    case 32: return launch_n<32>(inverse, ax, in, out, nlines, inner, s);
+    case 64: return launch_n<64>(inverse, ax, in, out, nlines, inner, s);
+    case 128: return launch_n<128>(inverse, ax, in, out, nlines, inner, s);
+    case 256: return launch_n<256>(inverse, ax, in, out, nlines, inner, s);
+    case 512: return launch_n<512>(inverse, ax, in, out, nlines, inner, s);
+    case 1024: return launch_n<1024>(inverse, ax, in, out, nlines, inner, s);
+    case 2048: return launch_n<2048>(inverse, ax, in, out, nlines, inner, s);
+    case 4096: return launch_n<4096>(inverse, ax, in, out, nlines, inner, s);
+    default: return fail(JT_ERR_ARG, "unsupported FFT length");
+  }
+}
+
+template <class T>
+jt_status upload(T **dst, const T *src, size_t count) {
+  if (count == 0) {
+    *dst = nullptr;
+    return JT_OK;
+  }
+  cudaError_t e = cudaMalloc((void **)dst, count * sizeof(T));
+  if (e != cudaSuccess) return fail(JT_ERR_ALLOC, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  e = cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(JT_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+  return JT_OK;
+}
+
+void free_device(jt_plan_s *p) {
+  if (p->device < 0) return;
+  DeviceGuard g(p->device);
+  for (int i = 0; i < 3; ++i) {
+    cudaFree(p->dev[i].u);
+    cudaFree(p->dev[i].v);
+    cudaFree(p->dev[i].tw);
+    cudaFree(p->dev[i].phiv);
+    cudaFree(p->dev[i].bstart);
+    p->dev[i] = AxisDevBuf();
+  }
+  cudaFree(p->stage_in);
+  cudaFree(p->stage_out);
+  p->stage_in = p->stage_out = nullptr;
+}
+
+jt_status upload_axis(jt_plan_s *p, int axis) {
+  const jt::AxisHost &h = p->host[axis];
+  const int64_t n = h.n, N = h.N;
+  const int r = h.r;
+  std::vector<double2> u((size_t)r * n), v((size_t)r * N), tw(N);
+  for (int l = 0; l < r; ++l) {
+    for (int64_t j = 0; j < n; ++j) {
+      const jt::cd z = h.u[(size_t)j * r + l];
+      u[(size_t)l * n + j] = make_double2(z.real(), z.imag());
+    }
+    for (int64_t k = 0; k < N; ++k) {
+      const jt::cd z = h.v[(size_t)l * N + k];
+      v[(size_t)l * N + k] = make_double2(z.real(), z.imag());
+    }
+  }
+  const long double PI_L = 3.141592653589793238462643383279502884L;
+  for (int64_t q = 0; q < N; ++q) {
+    long double ang = 2 * PI_L * (long double)q / (long double)N;
+    tw[q] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  jt_status s;
+  if ((s = upload(&p->dev[axis].u, u.data(), u.size())) != JT_OK) return s;
+  if ((s = upload(&p->dev[axis].v, v.data(), v.size())) != JT_OK) return s;
+  if ((s = upload(&p->dev[axis].tw, tw.data(), tw.size())) != JT_OK) return s;
+  if ((s = upload(&p->dev[axis].phiv, h.phiv.data(), h.phiv.size())) != JT_OK) return s;
+  if ((s = upload(&p->dev[axis].bstart, h.bstart.data(), h.bstart.size())) != JT_OK) return s;
+  return JT_OK;
+}
+
+bool overlaps_partially(const double *x, const double *y, int64_t count) {
+  if (x == y) return false;
+  const double *xe = x + count, *ye = y + count;
+  return x < ye && y < xe;
+}
+
+jt_status check_device_plan(const jt_plan_s *p) {
+  if (!p) return fail(JT_ERR_ARG, "null plan");
+  if (p->device < 0) return fail(JT_ERR_ARG, "host-only plan (opts.device == -2) cannot run device calls");
+  // surface an asynchronous fault from an earlier call
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(JT_ERR_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(e));
+  }
+  return JT_OK;
+}
+
+// Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
+jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
+  jt_status st = check_device_plan(p);
+  if (st != JT_OK) return st;
+  if (!in || !out) return fail(JT_ERR_ARG, "null data pointer");
+  if (overlaps_partially(in, out, p->total)) return fail(JT_ERR_ARG, "input and output partially overlap");
+  DeviceGuard g(p->device);
+  const double *src = in;
+  for (int axis = p->d - 1; axis >= 0; --axis) {
+    long long outer = 1, inner = 1;
+    for (int i = 0; i < axis; ++i) outer *= p->n[i];
+    for (int i = axis + 1; i < p->d; ++i) inner *= p->n[i];
+    if ((st = launch_axis(p, axis, inverse, src, out, outer, inner, s)) != JT_OK) return st;
+    src = out;
+  }
+  return JT_OK;
+}
+
+jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double *out_h, cudaStream_t s) {
+  jt_status st = check_device_plan(p);
+  if (st != JT_OK) return st;
+  if (!in_h || !out_h) return fail(JT_ERR_ARG, "null host pointer");
+  DeviceGuard g(p->device);
+  const size_t bytes = (size_t)p->total * sizeof(double);
+  if (!p->stage_in) {
+    if (cudaMalloc((void **)&p->stage_in, bytes) != cudaSuccess) return fail(JT_ERR_ALLOC, "staging cudaMalloc");
+    if (cudaMalloc((void **)&p->stage_out, bytes) != cudaSuccess) return fail(JT_ERR_ALLOC, "staging cudaMalloc");
+  }
+  JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in, in_h, bytes, cudaMemcpyHostToDevice, s));
+  if ((st = transform(p, inverse, p->stage_in, p->stage_out, s)) != JT_OK) return st;
+  JT_CUDA_TRY(cudaMemcpyAsync(out_h, p->stage_out, bytes, cudaMemcpyDeviceToHost, s));
+  JT_CUDA_TRY(cudaStreamSynchronize(s));
+  return JT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *jt_last_error(void) { return g_last_error.c_str(); }
+
+const char *jt_version(void) { return "jt 0.1 (sm_100a fused fp64 axis passes)"; }
+
+jt_status jt_default_opts(jt_opts *o) {
+  if (!o) return fail(JT_ERR_ARG, "null opts");
+  o->seed = 0;
+  o->k0 = 27;
+  o->rmax_init = 0;
+  o->q = 3;
+  o->sweeps = 2;
+  o->device = -1;
+  return JT_OK;
+}
+
+jt_status jt_plan(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
+                  const jt_opts *opts) {
+  if (!out) return fail(JT_ERR_ARG, "null out");
+  *out = nullptr;
+  if (d < 1 || d > 3) return fail(JT_ERR_ARG, "d must be 1, 2 or 3");
+  if (!n || !a || !b) return fail(JT_ERR_ARG, "null n/a/b");
+  if (!(eps >= 1e-15 && eps <= 1e-2)) return fail(JT_ERR_ARG, "eps must be in [1e-15, 1e-2]");
+  jt_opts o;
+  jt_default_opts(&o);
+  if (opts) o = *opts;
+  if (o.k0 < 0 || o.k0 > 32) return fail(JT_ERR_ARG, "k0 must be in [0, 32]");
+  for (int i = 0; i < d; ++i) {
+    if (n[i] < 2 || n[i] > 4096) return fail(JT_ERR_ARG, "n[i] must be in [2, 4096]");
+    if (!(a[i] > -1 && a[i] < 1 && b[i] > -1 && b[i] < 1))
+      return fail(JT_ERR_DOMAIN, "a, b must lie in (-1, 1) (PAPER.md:1000: not applicable outside)");
+  }
+  jt_plan_s *p = new (std::nothrow) jt_plan_s();
+  if (!p) return fail(JT_ERR_ALLOC, "plan allocation");
+  p->d = d;
+  p->eps = eps;
+  p->opts = o;
+  p->total = 1;
+  for (int i = 0; i < d; ++i) {
+    p->n[i] = n[i];
+    p->a[i] = a[i];
+    p->b[i] = b[i];
+    p->total *= n[i];
+  }
+  try {
+    for (int i = 0; i < d; ++i) {
+      // identical axes share the host computation
+      int same = -1;
+      for (int k = 0; k < i; ++k)
+        if (n[k] == n[i] && a[k] == a[i] && b[k] == b[i]) same = k;
+      if (same >= 0) {
+        p->host[i] = p->host[same];
+        continue;
+      }
+      std::string err;
+      jt_status s = jt::build_axis_host(p->host[i], n[i], a[i], b[i], eps, o, err);
+      if (s != JT_OK) {
+        delete p;
+        return fail(s, "axis " + std::to_string(i) + ": " + err);
+      }
+    }
+  } catch (const std::bad_alloc &) {
+    delete p;
+    return fail(JT_ERR_ALLOC, "host allocation during plan");
+  } catch (const std::exception &ex) {
+    delete p;
+    return fail(JT_ERR_NUMERIC, std::string("plan: ") + ex.what());
+  }
+  if (o.device != -2) {
+    int dev = o.device;
+    if (dev == -1 && cudaGetDevice(&dev) != cudaSuccess) {
+      delete p;
+      return fail(JT_ERR_CUDA, "no CUDA device");
+    }
+    p->device = dev;
+    DeviceGuard g(dev);
+    for (int i = 0; i < d; ++i) {
+      jt_status s = upload_axis(p, i);
+      if (s != JT_OK) {
+        std::string msg = g_last_error;
+        free_device(p);
+        delete p;
+        return fail(s, msg);
+      }
+    }
+  }
+  *out = p;
+  return JT_OK;
+}
+
+jt_status jt_forward(jt_plan_t p, const double *coeffs, double *values, void *stream) {
+  return transform(p, false, coeffs, values, (cudaStream_t)stream);
+}
+
+jt_status jt_inverse(jt_plan_t p, const double *values, double *coeffs, void *stream) {
+  return transform(p, true, values, coeffs, (cudaStream_t)stream);
+}
+
+jt_status jt_forward_host(jt_plan_t p, const double *coeffs_host, double *values_host, void *stream) {
+  return transform_host(p, false, coeffs_host, values_host, (cudaStream_t)stream);
+}
+
+jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs_host, void *stream) {
+  return transform_host(p, true, values_host, coeffs_host, (cudaStream_t)stream);
+}
+
+static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *in, double *out, int64_t outer,
+                            int64_t inner, void *stream) {
+  jt_status st = check_device_plan(p);
+  if (st != JT_OK) return st;
+  if (axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad axis");
+  if (!in || !out || outer < 0 || inner < 1) return fail(JT_ERR_ARG, "bad pointers / shape");
+  if (overlaps_partially(in, out, outer * inner * p->n[axis])) return fail(JT_ERR_ARG, "partial overlap");
+  DeviceGuard g(p->device);
+  return launch_axis(p, axis, inverse, in, out, outer, inner, (cudaStream_t)stream);
+}
+
+jt_status jt_forward_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer, int64_t inner,
+                          void *stream) {
+  return axis_entry(p, axis, false, in, out, outer, inner, stream);
+}
+
+jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer, int64_t inner,
+                          void *stream) {
+  return axis_entry(p, axis, true, in, out, outer, inner, stream);
+}
+
+jt_status jt_destroy(jt_plan_t p) {
+  if (!p) return JT_OK;
+  free_device(p);
+  delete p;
+  return JT_OK;
+}
+
+jt_status jt_plan_rank(jt_plan_t p, int axis, int *r) {
+  if (!p || !r || axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad args");
+  *r = p->host[axis].r;
+  return JT_OK;
+}
+
+jt_status jt_plan_info(jt_plan_t p, int axis, int64_t *n, int64_t *nfft, int *k0, int *r) {
+  if (!p || axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad args");
+  const jt::AxisHost &h = p->host[axis];
+  if (n) *n = h.n;
+  if (nfft) *nfft = h.N;
+  if (k0) *k0 = h.k0;
+  if (r) *r = h.r;
+  return JT_OK;
+}
+
+jt_status jt_plan_nodes(jt_plan_t p, int axis, double *t_host, double *w_host) {
+  if (!p || axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad args");
+  const jt::AxisHost &h = p->host[axis];
+  if (t_host) std::memcpy(t_host, h.t.data(), h.n * sizeof(double));
+  if (w_host) std::memcpy(w_host, h.w.data(), h.n * sizeof(double));
+  return JT_OK;
+}
+
+jt_status jt_plan_factors(jt_plan_t p, int axis, double *u_host, double *v_host, double *phiv_host,
+                          int32_t *bins_host) {
+  if (!p || axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad args");
+  const jt::AxisHost &h = p->host[axis];
+  if (u_host) std::memcpy(u_host, h.u.data(), h.u.size() * sizeof(jt::cd));
+  if (v_host) std::memcpy(v_host, h.v.data(), h.v.size() * sizeof(jt::cd));
+  if (phiv_host) std::memcpy(phiv_host, h.phiv.data(), h.phiv.size() * sizeof(double));
+  if (bins_host) std::memcpy(bins_host, h.bins.data(), h.bins.size() * sizeof(int32_t));
+  return JT_OK;
+}
+
+jt_status jt_plan_sigma(jt_plan_t p, int axis, double *sigma, int *count, int *rmax_used) {
+  if (!p || axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad args");
+  const jt::AxisHost &h = p->host[axis];
+  if (count) *count = (int)h.sigma.size();
+  if (rmax_used) *rmax_used = h.rmax_used;
+  if (sigma) std::memcpy(sigma, h.sigma.data(), h.sigma.size() * sizeof(double));
+  return JT_OK;
+}
+
+// Test hook (declared in include/jt_debug.h): P~_k, Q~_k by the plan's own route.
+jt_status jt_debug_modified_pq(double a, double b, int64_t nt, const double *t, int kmax, double *p_out,
+                               double *q_out) {
+  if (!t || !p_out || !q_out || nt < 0 || kmax < 0) return fail(JT_ERR_ARG, "bad args");
+  if (!(a > -1 && a < 1 && b > -1 && b < 1)) return fail(JT_ERR_DOMAIN, "a, b must lie in (-1, 1)");
+  jt::modified_pq(a, b, nt, t, kmax, p_out, q_out);
+  return JT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north star): relative l2 error <= 1e-10 against the oracle on the same seeded inputs
+(fp64), and forward->inverse round trip <= 1e-10.  The method's own error at eps = 1e-12 is ~1e-12.
+Full-size configs are checked on sampled outputs computed one by one by the oracle plus the round trip.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import seeded_inputs as si
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_1901_07275_b200 as jt
+
+TOL = 1e-10
+
+
+def relerr(x, ref):
+    return float(np.linalg.norm(np.ravel(x) - np.ravel(ref)) / np.linalg.norm(np.ravel(ref)))
+
+
+def gpu_forward(plan, x_np, inverse=False, inplace=False, stream=None):
+    x = torch.from_numpy(x_np).cuda()
+    if inplace:
+        out = x
+    else:
+        out = torch.empty_like(x)
+    (jt.jt_inverse if inverse else jt.jt_forward)(plan.handle, x, out, stream)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+# ragged and edge shapes: n <= k0 (dense-only), n = k0 + 1, non powers of two (FFT length N > n),
+# line counts that are not multiples of the CTA's line tile
+CASES_1D = [(2, 0.1, -0.2), (16, 0.3, 0.3), (27, -0.5, 0.5), (28, 0.25, -0.3), (64, 0.45, -0.45),
+            (100, -0.75, 0.2), (256, 0.1, -0.4), (333, 0.9, -0.9), (512, 0.25, -0.25), (777, 0.0, 0.0),
+            (1024, 0.25, -0.3), (2048, -0.3, 0.6), (3000, 0.2, 0.2), (4096, 0.45, -0.45)]
+
+
+@pytest.mark.parametrize("n,a,b", CASES_1D)
+def test_1d_forward_inverse(n, a, b):
+    p = jt.Plan(n, a, b, 1e-12)
+    x = si.gaussian((n,), seed=n)
+    y = gpu_forward(p, x)
+    assert relerr(y, oracle.forward(x, a, b)) <= TOL
+    z = gpu_forward(p, x, inverse=True)
+    assert relerr(z, oracle.inverse(x, a, b)) <= TOL
+    assert relerr(gpu_forward(p, y, inverse=True), x) <= TOL
+
+
+CASES_ND = [((256, 256), (0.1, -0.25), (-0.4, 0.35)),              # BASELINE config 2
+            ((100, 300), (0.3, -0.6), (0.2, 0.45)),
+            ((33, 7), (0.0, 0.5), (0.0, -0.5)),
+            ((4096, 16), (0.45, 0.0), (-0.45, 0.0)),
+            ((17, 2048), (-0.2, 0.7), (0.1, 0.3)),
+            ((64, 48, 40), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)),
+            ((5, 130, 9), (0.25, 0.25, 0.25), (-0.25, -0.25, -0.25)),
+            ((128, 128, 128), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1))]
+
+
+@pytest.mark.parametrize("shape,a,b", CASES_ND)
+def test_nd_forward_inverse(shape, a, b):
+    p = jt.Plan(shape, a, b, 1e-12)
+    x = si.gaussian(shape, seed=len(shape))
+    y = gpu_forward(p, x)
+    assert relerr(y, oracle.forward(x, a, b)) <= TOL
+    z = gpu_forward(p, x, inverse=True)
+    assert relerr(z, oracle.inverse(x, a, b)) <= TOL
+
+
+def test_config1_1d_1024():
+    c = si.CONFIGS["cfg1_1d_1024"]
+    p = jt.Plan(c["n"], c["a"], c["b"], c["eps"])
+    x = si.gaussian(c["n"], seed=0)
+    y = gpu_forward(p, x)
+    assert relerr(y, oracle.forward(x, c["a"], c["b"])) <= TOL
+    assert relerr(gpu_forward(p, y, inverse=True), x) <= TOL
+
+
+def test_config4_3d_256_full():
+    c = si.CONFIGS["cfg4_3d_256"]
+    p = jt.Plan(c["n"], c["a"], c["b"], c["eps"])
+    x = si.gaussian(c["n"], seed=0)
+    y = gpu_forward(p, x)
+    assert relerr(y, oracle.forward(x, c["a"], c["b"])) <= TOL
+    yi = si.gaussian(c["n"], seed=1)
+    assert relerr(gpu_forward(p, yi, inverse=True), oracle.inverse(yi, c["a"], c["b"])) <= TOL
+    assert relerr(gpu_forward(p, y, inverse=True), x) <= TOL
+
+
+@pytest.mark.parametrize("name", ["cfg3_2d_4096", "cfg5_3d_512"])
+def test_full_size_sampled(name):
+    """Full-size configs in the launch configuration bench.py times: sampled outputs vs the oracle's
+    one-by-one sums (forward_at / inverse_at), plus the round trip over the whole array."""
+    c = si.CONFIGS[name]
+    p = jt.Plan(c["n"], c["a"], c["b"], c["eps"])
+    x = si.gaussian(c["n"], seed=0)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    jt.jt_forward(p.handle, xd, yd)
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy()
+    idx = si.sample_indices(c["n"], 24, seed=3)
+    ref = oracle.forward_at(x, c["a"], c["b"], idx)
+    got = y[tuple(idx.T)]
+    assert np.max(np.abs(got - ref)) <= TOL * np.linalg.norm(ref) / np.sqrt(len(ref)) * 10
+    assert relerr(got, ref) <= TOL
+    # round trip over the whole array (orthogonality: Phi^T Phi = I)
+    zd = torch.empty_like(xd)
+    jt.jt_inverse(p.handle, yd, zd)
+    torch.cuda.synchronize()
+    assert relerr(zd.cpu().numpy(), x) <= TOL
+    if c["inverse"]:
+        idx2 = si.sample_indices(c["n"], 24, seed=4)
+        ref2 = oracle.inverse_at(y, c["a"], c["b"], idx2)
+        got2 = zd.cpu().numpy()[tuple(idx2.T)]
+        assert relerr(got2, ref2) <= TOL
+
+
+def test_inplace_and_stream_and_determinism():
+    shape, a, b = (96, 200), (0.3, -0.1), (0.2, 0.4)
+    p = jt.Plan(shape, a, b, 1e-12)
+    x = si.gaussian(shape, seed=9)
+    y1 = gpu_forward(p, x)
+    y2 = gpu_forward(p, x, inplace=True)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        jt.jt_forward(p.handle, xd, yd, s)
+    s.synchronize()
+    np.testing.assert_array_equal(y1, y2)
+    np.testing.assert_array_equal(y1, yd.cpu().numpy())
+
+
+def test_host_entry_points_match_device():
+    shape, a, b = (64, 64, 64), (0.1, 0.2, 0.3), (-0.1, -0.2, -0.3)
+    p = jt.Plan(shape, a, b, 1e-12)
+    x = si.gaussian(shape, seed=2)
+    np.testing.assert_array_equal(p.forward_host(x), gpu_forward(p, x))
+    np.testing.assert_array_equal(p.inverse_host(x), gpu_forward(p, x, inverse=True))
+
+
+def test_axis_entry_points_compose():
+    shape, a, b = (40, 72, 33), (0.1, -0.6, 0.5), (0.0, 0.3, -0.2)
+    p = jt.Plan(shape, a, b, 1e-12)
+    x = si.gaussian(shape, seed=5)
+    xd = torch.from_numpy(x).cuda()
+    w = xd.clone()
+    for ax in (0, 1, 2):  # any axis order (the Kronecker factors commute)
+        outer = int(np.prod(shape[:ax]))
+        inner = int(np.prod(shape[ax + 1:]))
+        jt.jt_forward_axis(p.handle, ax, w, w, outer, inner)
+    torch.cuda.synchronize()
+    assert relerr(w.cpu().numpy(), oracle.forward(x, a, b)) <= TOL
+
+
+def test_partial_overlap_rejected():
+    p = jt.Plan(64, 0.1, 0.1, 1e-12)
+    buf = torch.zeros(128, dtype=torch.float64, device="cuda")
+    with pytest.raises(jt.JTError) as ei:
+        jt.jt_forward(p.handle, buf[:64], buf[8:72])
+    assert ei.value.status == jt.JT_ERR_ARG
