@@ -1,0 +1,329 @@
+"""Benchmark: fp64 uniform Jacobi transform (arXiv 1901.07275 hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (slab-distributed, NCCL all-to-all)
+
+Workload (BASELINE.json configs[4], the largest grid, the one the metric's 1/2/4/8-GPU scaling is
+quoted on): 3D uniform forward transform, 512 x 512 x 512 (134M fp64 coefficients), (a,b) =
+(0.25,-0.25) on every axis, eps = 1e-12, coefficients iid N(0,1) from seed 0.  A step = one whole
+forward transform (all three fused axis passes; with N > 1 also the all-to-all).  Inputs (1.07 GB) are
+larger than L2 (126 MB), so no extra flush is needed between steps.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the only reference that
+exists for this paper: BASELINE.json published = {}) on host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import seeded_inputs as si  # noqa: E402
+
+METRIC = "Jacobi-transform coefficients/sec (fp64, 2D/3D) and % of HBM roofline at 1/2/4/8 GPUs"
+FP64_PEAK_TFLOPS = 37.0   # measured DFMA peak (profiles/fp64_peak_r01.json); derived 148*64*2*1.965 GHz = 37.2
+K0 = 27
+
+
+def algorithmic_flops_per_point(n: int, r: int, k0: int = K0) -> float:
+    """per axis pass per point r (5 log2 N + 6) + 2 k0 (conventional FFT count)."""
+    return r * (5 * np.log2(n) + 6) + 2 * k0
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.gpu = gpu_index
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        mhz, maxmhz, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                mhz.append(float(f[1]))
+                maxmhz.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": max(maxmhz) if maxmhz else None,
+                "reasons": sorted(reasons), "samples": len(mhz), "power_w_max": max(power) if power else None}
+
+
+def cpu_oracle_rate(cfg, max_seconds: float = 30.0):
+    """The oracle (oracle/jacobi.py) as it stands, on this host's cores: full forward of the config if it
+    fits the time bound, else a slab of it.  Returns (coefficients/s, sample description, threads)."""
+    import oracle
+    shape, a, b = cfg["n"], cfg["a"], cfg["b"]
+    for ax in range(len(shape)):  # Phi construction is the oracle's "fac"; not part of the apply rate
+        oracle.phi(shape[ax], a[ax], b[ax])
+    x = si.gaussian(shape, seed=0)
+    t0 = time.perf_counter()
+    oracle.forward(x, a, b)
+    dt = time.perf_counter() - t0
+    threads = os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max(int(i.get("num_threads", 1)) for i in threadpool_info()) or threads
+    except Exception:
+        pass
+    desc = f"full {'x'.join(map(str, shape))} forward (dense separable mode products, fp64 BLAS), 1 run, {dt:.1f} s"
+    return float(np.prod(shape)) / dt, desc, threads
+
+
+def run_reference(args, cfg, rank: int):
+    """--impl reference: the CPU oracle timed on the host (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    shape, a, b = cfg["n"], cfg["a"], cfg["b"]
+    for ax in range(len(shape)):
+        oracle.phi(shape[ax], a[ax], b[ax])
+    # Bounded sample per step (1/8 of the transform's work): the last d-1 axis passes on an x-slab of
+    # n0/8 planes, and the axis-0 pass on the full-height block of the first n1/8 columns.  Both have the
+    # exact per-point cost of the full transform's passes.
+    x = si.gaussian(shape, seed=0)
+    slab = max(1, shape[0] // 8)
+    xs = np.ascontiguousarray(x[:slab])
+
+    def step():
+        y = oracle.forward_axes(xs, a, b, axes=list(range(len(shape) - 1, 0, -1)))
+        # axis 0 on the full-height columns of the first slab/8 columns of axis 1 (bounded work)
+        cols = np.ascontiguousarray(x[:, : max(1, shape[1] // 8)])
+        oracle.forward_axes(cols, a, b, axes=[0])
+        return y
+
+    pts_step = xs.size + (x[:, : max(1, shape[1] // 8)].size if len(shape) > 1 else 0)
+    pass_pts = xs.size * (len(shape) - 1) + (x[:, : max(1, shape[1] // 8)].size if len(shape) > 1 else 0)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    # rate in coefficients/s of the whole transform: (axis-pass points per second) / d
+    value = pass_pts / dt / len(shape)
+    threads = os.cpu_count()
+    sample = (f"per step 1/8 of the transform's work: axes {len(shape)-1}..1 on an x-slab of {slab} planes + "
+              f"axis 0 on the first n1/8 columns ({pass_pts} axis-pass points); value = axis-pass points/s / d")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "coefficients/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1), seed 0",
+            "config": config_block(args, cfg, None),
+            "cpu_baseline": {"value": value, "unit": "coefficients/s", "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "coefficients/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, cfg, ranks):
+    return {"workload": f"{args.config}: {'x'.join(map(str, cfg['n']))} uniform forward, (a,b)="
+                        f"{list(zip(cfg['a'], cfg['b']))}, eps={cfg['eps']}",
+            "model": "none (transform)", "global_batch": 1, "seq_len": int(np.prod(cfg["n"])),
+            "ranks_per_axis": ranks, "k0": K0, "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
+            "l2_policy": "inputs (8 B x prod(n)) larger than the 126 MB L2; no extra flush"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg5_3d_512", choices=list(si.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = si.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    import paper_1901_07275_b200 as jt
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        from paper_1901_07275_b200.dist import SlabPlan
+    shape, a, b, eps = cfg["n"], cfg["a"], cfg["b"], cfg["eps"]
+    d = len(shape)
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        plan = jt.Plan(shape, a, b, eps)
+        ranks = [plan.rank(i) for i in range(d)]
+        x = torch.from_numpy(si.gaussian(shape, seed=0)).cuda()
+        y = torch.empty_like(x)
+        strides = []
+        for ax in range(d - 1, -1, -1):
+            strides.append((ax, int(np.prod(shape[:ax])), int(np.prod(shape[ax + 1:]))))
+
+        def step(evs=None):
+            src = x
+            for i, (ax, outer, inner) in enumerate(strides):
+                if evs is not None:
+                    evs[i].record(stream)
+                jt.jt_forward_axis(plan.handle, ax, src, y, outer, inner, stream)
+                src = y
+            if evs is not None:
+                evs[-1].record(stream)
+        launches_per_step = d
+        local_points = int(np.prod(shape))
+    else:
+        plan = SlabPlan(shape, a, b, eps, dist)
+        ranks = plan.ranks
+        x = plan.local_input(torch.from_numpy(si.gaussian(shape, seed=0)))
+        step = plan.make_forward_step(x)
+        launches_per_step = plan.launches_per_step
+        local_points = x.numel()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    time.sleep(0.3)
+    nev = (d + 1) if world == 1 else 2
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        if world == 1:
+            step(evs[k])
+        else:
+            step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms_total = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    total_points = float(np.prod(shape))
+    value = total_points / (ms_step * 1e-3)
+
+    roofline = None
+    per_axis_ms = None
+    if world == 1:
+        per_axis = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(d)] for k in range(args.steps)])
+        per_axis_ms = per_axis.mean(axis=0)  # in launch order (axis d-1 first)
+        # dominant kernel: the fused forward axis pass (all d launches are this kernel; take the slowest axis)
+        i_dom = int(np.argmax(per_axis_ms))
+        ax_dom = strides[i_dom][0]
+        n_ax = shape[ax_dom]
+        flops = algorithmic_flops_per_point(n_ax, ranks[ax_dom]) * total_points
+        achieved = flops / (per_axis_ms[i_dom] * 1e-3) / 1e12
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+                prof = json.load(f)
+            traffic = prof.get(args.config, {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        hbm_bytes = 16.0 * total_points
+        roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "kernel": f"fwd_axis_kernel<N={shape[ax_dom]}> (axis {ax_dom})",
+                    "flops_per_launch": flops,
+                    "per_axis_ms_launch_order": [round(float(v), 4) for v in per_axis_ms],
+                    "hbm_algorithmic_GBps": hbm_bytes / (per_axis_ms[i_dom] * 1e-3) / 1e9,
+                    "hbm_frac_of_measured": hbm_bytes / (per_axis_ms[i_dom] * 1e-3) / 1e9 / load_peaks()["hbm_gbs"],
+                    "peak_source": "FP64 DFMA measured 37.0 TF/s burst = sustained (profiles/fp64_peak_r01.json); "
+                                   "148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 derived"}
+
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        xh = torch.from_numpy(si.gaussian(shape, seed=0)).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        xn, yn = xh.numpy(), yh.numpy()
+        plan.forward_host(xn, yn, stream)  # warm the staging buffers
+        e2e_steps = max(3, min(args.steps, 5))
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(e2e_steps):
+            plan.forward_host(xn, yn, stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = t0.elapsed_time(t1) / e2e_steps
+        e2e = {"value": total_points / (ms_e2e * 1e-3), "unit": "coefficients/s",
+               "h2d_bytes_per_step": int(8 * total_points), "d2h_bytes_per_step": int(8 * total_points),
+               "ms_per_step": ms_e2e, "api": "jt_forward_host (pinned host buffers; H2D + 3 axis passes + D2H)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, desc, threads = cpu_oracle_rate(cfg)
+        cpu = {"value": v, "unit": "coefficients/s", "cores": threads, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "coefficients/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) fp64, numpy PCG64 seed 0",
+                "config": config_block(args, cfg, ranks), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
