@@ -1,5 +1,5 @@
 // In-register fp64 complex DFT building blocks (positive exponent, unnormalised):
-//     X[s] = sum_r x[r] e^{+2 pi i r s / M},   M in {2, 4, 8, 16}
+//     X[s] = sum_r x[r] e^{+2 pi i r s / M},   M in {2, 4, 8, 16, 32}
 // Used as the radix-M butterflies of the Stockham passes of the fused axis kernels (fused_axis.cuh).
 // The sign is the paper's: F_n is "a row permutation of an inverse DFT matrix",
 // applied as r "inverse FFTs"; the inverse transform uses the same sign (eq:oneJinv,
@@ -10,33 +10,36 @@ namespace jtk {
 
 #define JT_DEV __device__ __forceinline__
 
-// cos / sin of 2 pi k / 16, k = 0..15 (exact decimal expansions, rounded by the compiler).
-JT_DEV double cos16(int k) {
-  constexpr double c1 = 0.92387953251128675612818318939678828682, c2 = 0.70710678118654752440084436210484903928,
-                   c3 = 0.38268343236508977172845998403039886676;
-  constexpr double C[16] = {1.0, c1, c2, c3, 0.0, -c3, -c2, -c1, -1.0, -c1, -c2, -c3, 0.0, c3, c2, c1};
-  return C[k & 15];
+// cos / sin of 2 pi k / 32, k = 0..31 (decimal expansions rounded by the compiler).
+JT_DEV double cos32(int k) {
+  constexpr double c1 = 0.98078528040323044912618223613424, c2 = 0.92387953251128675612818318939679,
+                   c3 = 0.83146961230254523707878837761791, c4 = 0.70710678118654752440084436210485,
+                   c5 = 0.55557023301960222474283081394853, c6 = 0.38268343236508977172845998403040,
+                   c7 = 0.19509032201612826784828486847702;
+  constexpr double C[32] = {1.0, c1, c2, c3, c4, c5, c6, c7, 0.0, -c7, -c6, -c5, -c4, -c3, -c2, -c1,
+                            -1.0, -c1, -c2, -c3, -c4, -c5, -c6, -c7, 0.0, c7, c6, c5, c4, c3, c2, c1};
+  return C[k & 31];
 }
-JT_DEV double sin16(int k) { return cos16(k - 4); }
+JT_DEV double sin32(int k) { return cos32(k - 8); }
 
-// (re, im) *= e^{+2 pi i k / M} for a k, M that are compile-time constants after unrolling; the
-// trivial angles (multiples of pi/4) are special-cased so no multiply by 0 or 1 is emitted.
+// (re, im) *= e^{+2 pi i k / M} for k, M compile-time constants after unrolling (M | 32); the angles
+// that are multiples of pi/4 are special-cased so no multiply by 0 or +-1 is emitted.
 template <int M>
 JT_DEV void twc(int k, double &re, double &im) {
-  static_assert(16 % M == 0, "M must divide 16");
-  const int k16 = ((k * (16 / M)) % 16 + 16) % 16;
+  static_assert(32 % M == 0, "M must divide 32");
+  const int k32 = ((k * (32 / M)) % 32 + 32) % 32;
   constexpr double h = 0.70710678118654752440084436210484903928;
-  switch (k16) {
+  switch (k32) {
     case 0: break;
-    case 4: { double t = re; re = -im; im = t; } break;                       // * i
-    case 8: re = -re; im = -im; break;                                        // * -1
-    case 12: { double t = re; re = im; im = -t; } break;                      // * -i
-    case 2: { double t = (re - im) * h; im = (re + im) * h; re = t; } break;  // (1+i)/sqrt2
-    case 6: { double t = -(re + im) * h; im = (re - im) * h; re = t; } break; // (-1+i)/sqrt2
-    case 10: { double t = (im - re) * h; im = -(re + im) * h; re = t; } break;// (-1-i)/sqrt2
-    case 14: { double t = (re + im) * h; im = (im - re) * h; re = t; } break; // (1-i)/sqrt2
+    case 8: { double t = re; re = -im; im = t; } break;                        // * i
+    case 16: re = -re; im = -im; break;                                        // * -1
+    case 24: { double t = re; re = im; im = -t; } break;                       // * -i
+    case 4: { double t = (re - im) * h; im = (re + im) * h; re = t; } break;   // (1+i)/sqrt2
+    case 12: { double t = -(re + im) * h; im = (re - im) * h; re = t; } break; // (-1+i)/sqrt2
+    case 20: { double t = (im - re) * h; im = -(re + im) * h; re = t; } break; // (-1-i)/sqrt2
+    case 28: { double t = (re + im) * h; im = (im - re) * h; re = t; } break;  // (1-i)/sqrt2
     default: {
-      const double c = cos16(k16), s = sin16(k16);
+      const double c = cos32(k32), s = sin32(k32);
       double t = re * c - im * s;
       im = fma(re, s, im * c);
       re = t;
@@ -63,6 +66,9 @@ JT_DEV void dft4(double *xr, double *xi) {
   xr[3] = t1r + t3i; xi[3] = t1i - t3r;  // t1 - i t3
 }
 
+template <int M>
+JT_DEV void dft(double *xr, double *xi);
+
 // Cooley-Tukey M = N1 N2 in registers: n = N2 n1 + n2, k = k1 + N1 k2.
 //   Y[k1][n2] = DFT_N1 over n1 of x[N2 n1 + n2];  Y *= w_M^{n2 k1};  X[k1 + N1 k2] = DFT_N2 over n2.
 template <int N1, int N2>
@@ -74,7 +80,7 @@ JT_DEV void dft_ct(double *xr, double *xi) {
     double ar[N1], ai[N1];
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) { ar[n1] = xr[N2 * n1 + n2]; ai[n1] = xi[N2 * n1 + n2]; }
-    if constexpr (N1 == 2) dft2(ar, ai); else dft4(ar, ai);
+    dft<N1>(ar, ai);
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) {
       twc<M>(n2 * k1, ar[k1], ai[k1]);
@@ -87,7 +93,7 @@ JT_DEV void dft_ct(double *xr, double *xi) {
     double br[N2], bi[N2];
 #pragma unroll
     for (int n2 = 0; n2 < N2; ++n2) { br[n2] = yr[k1 * N2 + n2]; bi[n2] = yi[k1 * N2 + n2]; }
-    if constexpr (N2 == 2) dft2(br, bi); else dft4(br, bi);
+    dft<N2>(br, bi);
 #pragma unroll
     for (int k2 = 0; k2 < N2; ++k2) { xr[k1 + N1 * k2] = br[k2]; xi[k1 + N1 * k2] = bi[k2]; }
   }
@@ -104,8 +110,10 @@ JT_DEV void dft(double *xr, double *xi) {
     dft_ct<2, 4>(xr, xi);
   } else if constexpr (M == 16) {
     dft_ct<4, 4>(xr, xi);
+  } else if constexpr (M == 32) {
+    dft_ct<4, 8>(xr, xi);
   } else {
-    static_assert(M <= 16, "radix too large");
+    static_assert(M <= 32, "radix too large");
   }
 }
 
