@@ -11,7 +11,7 @@
 #include <new>
 #include <string>
 
-#include "fused_axis.cuh"
+#include "axis_kernels.cuh"
 #include "jt_internal.h"
 
 namespace {
@@ -30,9 +30,10 @@ jt_status fail(jt_status s, const std::string &msg) {
   } while (0)
 
 struct AxisDevBuf {
-  double2 *u = nullptr, *v = nullptr, *tw = nullptr;
-  double *phiv = nullptr;
+  double2 *ub = nullptr, *v = nullptr, *tw = nullptr;
+  double *phivb = nullptr;
   int *bstart = nullptr;
+  int maxr = 0;  // row slots per bin in ub / phivb (template MAXR of the kernels)
 };
 
 // Restores the caller's current device on scope exit.
@@ -72,55 +73,68 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
   ax.N = (int)h.N;
   ax.k0 = h.k0;
   ax.r = h.r;
-  ax.u = p->dev[axis].u;
+  ax.nbins = (int)(h.N / 2 + 1);
   ax.v = p->dev[axis].v;
-  ax.phiv = p->dev[axis].phiv;
+  ax.ub = p->dev[axis].ub;
+  ax.phivb = p->dev[axis].phivb;
   ax.bstart = p->dev[axis].bstart;
   ax.tw = p->dev[axis].tw;
   return ax;
 }
 
-template <int N>
-constexpr int lines_for() {
-  return N <= 128 ? 32 : (N == 256 ? 16 : (N == 512 ? 8 : (N == 1024 ? 4 : (N == 2048 ? 2 : 1))));
+// Radix of the first (register) pass for FFT length N: one SMEM exchange per term for N <= 1024
+// (16x16, 32x16, 32x32), two for 2048 and 4096 (32x32x2, 32x32x4); see DESIGN.md "Kernels".
+// MAXR = 4 (more than two nodes in some bin: only for (a, b) near the ends of (-1, 1)) always uses
+// radix 16, whose accumulators fit in registers.
+template <int N, int MAXR>
+constexpr int radix_for() {
+  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : 32)));
 }
+int radix_of(int64_t N, int maxr) { return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : 32))); }
 
-template <int N>
-jt_status launch_n(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                   long long inner, cudaStream_t s) {
-  constexpr int R = 16;
-  constexpr int LINES = lines_for<N>();
-  using G = jtk::Geo<N, R, LINES>;
-  const size_t smem = G::smem_bytes(ax.k0);
-  const long long blocks = (nlines + LINES - 1) / LINES;
+template <class C>
+jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
+                     long long inner, cudaStream_t s) {
+  const size_t smem = C::smem_bytes();
+  const long long lines_per_cta = (long long)C::GPC * C::LG;
+  const long long blocks = (nlines + lines_per_cta - 1) / lines_per_cta;
   if (blocks == 0) return JT_OK;
+  if (blocks > 0x7fffffffLL) return fail(JT_ERR_ARG, "too many lines for one launch");
   if (inverse) {
-    auto kern = jtk::inv_axis_kernel<N, R, LINES>;
+    auto kern = jtk::inv_axis_kernel<C>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)blocks, G::NT, smem, s>>>(ax, in, out, nlines, inner);
+    kern<<<(unsigned)blocks, C::NT, smem, s>>>(ax, in, out, nlines, inner);
   } else {
-    auto kern = jtk::fwd_axis_kernel<N, R, LINES>;
+    auto kern = jtk::fwd_axis_kernel<C>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)blocks, G::NT, smem, s>>>(ax, in, out, nlines, inner);
+    kern<<<(unsigned)blocks, C::NT, smem, s>>>(ax, in, out, nlines, inner);
   }
   JT_CUDA_TRY(cudaGetLastError());
   return JT_OK;
 }
 
+template <int N>
+jt_status launch_n(bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
+                   long long inner, cudaStream_t s) {
+  if (maxr <= 2) return launch_cfg<jtk::Cfg<N, radix_for<N, 2>(), 2>>(inverse, ax, in, out, nlines, inner, s);
+  return launch_cfg<jtk::Cfg<N, radix_for<N, 4>(), 4>>(inverse, ax, in, out, nlines, inner, s);
+}
+
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
                       long long inner, cudaStream_t s) {
   jtk::AxisDev ax = axis_dev(p, axis);
+  const int maxr = p->dev[axis].maxr;
   const long long nlines = outer * inner;
   switch (ax.N) {
-    case 16: return launch_n<16>(inverse, ax, in, out, nlines, inner, s);
-    case 32: return launch_n<32>(inverse, ax, in, out, nlines, inner, s);
-    case 64: return launch_n<64>(inverse, ax, in, out, nlines, inner, s);
-    case 128: return launch_n<128>(inverse, ax, in, out, nlines, inner, s);
-    case 256: return launch_n<256>(inverse, ax, in, out, nlines, inner, s);
-    case 512: return launch_n<512>(inverse, ax, in, out, nlines, inner, s);
-    case 1024: return launch_n<1024>(inverse, ax, in, out, nlines, inner, s);
-    case 2048: return launch_n<2048>(inverse, ax, in, out, nlines, inner, s);
-    case 4096: return launch_n<4096>(inverse, ax, in, out, nlines, inner, s);
+    case 16: return launch_n<16>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 32: return launch_n<32>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 64: return launch_n<64>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 128: return launch_n<128>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 256: return launch_n<256>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 512: return launch_n<512>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 1024: return launch_n<1024>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 2048: return launch_n<2048>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 4096: return launch_n<4096>(inverse, maxr, ax, in, out, nlines, inner, s);
     default: return fail(JT_ERR_ARG, "unsupported FFT length");
   }
 }
@@ -142,10 +156,10 @@ void free_device(jt_plan_s *p) {
   if (p->device < 0) return;
   DeviceGuard g(p->device);
   for (int i = 0; i < 3; ++i) {
-    cudaFree(p->dev[i].u);
+    cudaFree(p->dev[i].ub);
     cudaFree(p->dev[i].v);
     cudaFree(p->dev[i].tw);
-    cudaFree(p->dev[i].phiv);
+    cudaFree(p->dev[i].phivb);
     cudaFree(p->dev[i].bstart);
     p->dev[i] = AxisDevBuf();
   }
@@ -156,29 +170,57 @@ void free_device(jt_plan_s *p) {
 
 jt_status upload_axis(jt_plan_s *p, int axis) {
   const jt::AxisHost &h = p->host[axis];
-  const int64_t n = h.n, N = h.N;
-  const int r = h.r;
-  std::vector<double2> u((size_t)r * n), v((size_t)r * N), tw(N);
-  for (int l = 0; l < r; ++l) {
-    for (int64_t j = 0; j < n; ++j) {
-      const jt::cd z = h.u[(size_t)j * r + l];
-      u[(size_t)l * n + j] = make_double2(z.real(), z.imag());
+  const int64_t N = h.N;
+  const int r = h.r, k0 = h.k0;
+  const int64_t nbins = N / 2 + 1;
+  // bin-major layouts (rows of bin m in slots c < MAXR, zero padded) so that a thread owning bin m
+  // reads u~ and W V of all its rows with unit-stride vector loads
+  int maxr = 0;
+  for (int64_t m = 0; m < nbins; ++m) maxr = std::max(maxr, h.bstart[m + 1] - h.bstart[m]);
+  if (maxr > 4) return fail(JT_ERR_NUMERIC, "more than 4 nodes share one FFT bin");
+  const int MAXR = maxr <= 2 ? 2 : 4;
+  p->dev[axis].maxr = MAXR;
+  std::vector<double2> ub((size_t)r * nbins * MAXR, make_double2(0.0, 0.0)), v((size_t)r * N), tw(N);
+  std::vector<double> phivb((size_t)std::max(k0, 1) * nbins * MAXR, 0.0);
+  for (int64_t m = 0; m < nbins; ++m) {
+    for (int c = 0; c < h.bstart[m + 1] - h.bstart[m]; ++c) {
+      const int64_t j = h.bstart[m] + c;
+      for (int l = 0; l < r; ++l) {
+        const jt::cd z = h.u[(size_t)j * r + l];
+        ub[((size_t)l * nbins + m) * MAXR + c] = make_double2(z.real(), z.imag());
+      }
+      for (int k = 0; k < k0; ++k) phivb[((size_t)k * nbins + m) * MAXR + c] = h.phiv[(size_t)j * k0 + k];
     }
+  }
+  for (int l = 0; l < r; ++l) {
     for (int64_t k = 0; k < N; ++k) {
       const jt::cd z = h.v[(size_t)l * N + k];
       v[(size_t)l * N + k] = make_double2(z.real(), z.imag());
     }
   }
+  // per-pass twiddle tables (jtk::TwOff): for each pass after the first, at sub-size NS with radix RS,
+  // entries (r-1) NS + j = e^{+2 pi i j r / (NS RS)}, computed in long double and rounded once
   const long double PI_L = 3.141592653589793238462643383279502884L;
-  for (int64_t q = 0; q < N; ++q) {
-    long double ang = 2 * PI_L * (long double)q / (long double)N;
-    tw[q] = make_double2((double)cosl(ang), (double)sinl(ang));
+  tw.clear();
+  {
+    const int R = radix_of(N, MAXR);
+    int64_t NS = std::min<int64_t>(N, R);
+    while (NS < N) {
+      const int64_t RS = std::min<int64_t>(N / NS, R);
+      for (int64_t r = 1; r < RS; ++r)
+        for (int64_t j = 0; j < NS; ++j) {
+          const long double ang = 2 * PI_L * (long double)(j * r) / (long double)(NS * RS);
+          tw.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+        }
+      NS *= RS;
+    }
+    if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
   }
   jt_status s;
-  if ((s = upload(&p->dev[axis].u, u.data(), u.size())) != JT_OK) return s;
+  if ((s = upload(&p->dev[axis].ub, ub.data(), ub.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].v, v.data(), v.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].tw, tw.data(), tw.size())) != JT_OK) return s;
-  if ((s = upload(&p->dev[axis].phiv, h.phiv.data(), h.phiv.size())) != JT_OK) return s;
+  if ((s = upload(&p->dev[axis].phivb, phivb.data(), phivb.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].bstart, h.bstart.data(), h.bstart.size())) != JT_OK) return s;
   return JT_OK;
 }
