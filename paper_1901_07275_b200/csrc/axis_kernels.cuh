@@ -1,16 +1,14 @@
-// Fused axis-pass kernels, warp-group design (K4 forward, K5 inverse).
+// Fused axis-pass kernels (K4 forward, K5 inverse).
 //
 // Every line along the transformed axis is one of the paper's "n^{d-1} 1D transforms" (PAPER.md:676,
-// 724).  A GROUP of threads owns LG complete lines (LG = 32 / TPL lines per warp when a line needs
-// TPL <= 32 threads, else one line spread over GW = TPL / 32 warps) and computes, entirely on chip,
+// 724).  A GROUP of threads owns LG complete lines (TPL threads per line, thread gt = vt LG + line) and
+// computes, entirely on chip,
 //
 //   forward (eq:oneJ):    y = W V a_V  +  Re sum_{l<r} D_{u~_l} F_N D_{v_l} a_G
 //   inverse (eq:oneJinv): a_V = (W V)^T y,  a_G = Re sum_{l<r} D_{v_l} F_N^T D_{u~_l} y
 //
-// with ONE HBM read and ONE HBM write of each line per axis pass (all r rank terms batched in the pass,
-// north star: "batches several rank terms per pass to cut HBM round trips").  Groups never wait on one
-// another: the only barriers are __syncwarp (GW == 1) or a named barrier of the group's GW warps, so the
-// load / FFT / exchange phases of different groups on one SM overlap freely.
+// with ONE HBM read and ONE HBM write of each line per axis pass: all r rank terms are batched in the
+// pass (north star: "batches several rank terms per pass to cut HBM round trips").
 //
 // Per rank term l (registers unless noted):
 //   forward:  x[k] = v_l[k] a[k]                               (A1: column scale + pack)
@@ -22,13 +20,22 @@
 //             B = F_N b                                        (same sign)
 //             a[k] += Re(v_l[k] B[k])
 //
-// Register ownership (thread vt of TPL on its line): first-pass inputs at positions vt + r TPL (r < R);
-// last-pass outputs at v + s (N / RS_L), v = vt + i TPL.  The forward keeps its accumulators y per OUTPUT
-// BIN of the last pass (only bins m <= N/2 are ever read, t in (0, pi), so the dead half of the last
-// butterflies is removed by the compiler); the inverse keeps its y per INPUT bin of the first pass.
-// Both hold at most R/2 + 1 bins x MAXR rows per thread.
+// Execution structure:
+//   * Persistent CTAs (one per SM) of GPC independent groups loop over batches of GPC x LG lines.
+//   * The per-term factors (v_l: N complex; u~_l: MAXR x (N/2+1) complex) are streamed by the TMA
+//     bulk-copy engine into a 2-stage SMEM ring shared by the CTA's groups (mbarrier full/empty pairs,
+//     thread 0 is the producer).  Measured on B200 (tools/l1_probe.cu): an LDG.128 costs the L1 data
+//     pipe 4 cycles per warp whatever the address sharing and misses L1 here (SMEM takes it), while a
+//     broadcast LDS.128 costs ~2; the ring turns long-latency global factor loads into short SMEM ones.
+//   * Groups synchronise only among themselves (__syncwarp, or a named barrier of the group's warps), so
+//     the FP64-heavy FFT phases of one group overlap the SMEM-heavy exchange phases of another.
+//   * Register ownership (thread vt of TPL on its line): first-pass inputs at positions vt + r TPL
+//     (r < R); last-pass outputs at v + s (N / RS_L), v = vt + i TPL.  The forward keeps its y per OUTPUT
+//     bin of the last pass (only bins m <= N/2 are read, t in (0, pi), so the dead half of the last
+//     butterflies is removed by the compiler); the inverse keeps its y per INPUT bin of the first pass.
 #pragma once
 #include <cuda_runtime.h>
+#include <stdint.h>
 
 #include "fft_regs.cuh"
 
@@ -41,14 +48,15 @@ struct AxisDev {
   int r;      // rank (FFT terms per line)
   int nbins;  // N / 2 + 1
   const double2 *v;      // r x N        v_l[k] at v[l N + k] (zero for k < k0 and k >= n)
-  const double2 *ub;     // r x nbins x MAXR   u~_l of row bstart[m] + c at ub[(l nbins + m) MAXR + c] (0-padded)
-  const double *phivb;   // k0 x nbins x MAXR  (W V)[bstart[m] + c, k] at phivb[(k nbins + m) MAXR + c] (0-padded)
+  const double2 *ub;     // r x MAXR x nbins   u~_l of row bstart[m] + c at ub[(l MAXR + c) nbins + m] (0-padded)
+  const double *phivb;   // k0 x MAXR x nbins  (W V)[bstart[m] + c, k] at phivb[(k MAXR + c) nbins + m] (0-padded)
   const int *bstart;     // nbins + 1 row offsets: rows of bin m are bstart[m] .. bstart[m+1]-1
   const double2 *tw;     // per-pass twiddle tables, see TwOff (pass NS, radix RS: (RS-1) NS entries,
                          // entry (r-1) NS + j = e^{+2 pi i j r / (NS RS)})
 };
 
 constexpr int K0MAX = 32;
+constexpr int SMEM_LIMIT = 227 * 1024;
 
 // Radix of the Stockham pass that starts at sub-transform size NS.
 template <int N, int R, int NS>
@@ -77,34 +85,47 @@ template <int N, int R, int NS>
 struct TwOff<N, R, NS, N> {
   static constexpr int value = 0;
 };
-template <int N, int R>
-constexpr int tw_entries() { return TwOff<N, R, N>::value; }
 
 template <int N_, int R_, int MAXR_>
 struct Cfg {
   static constexpr int N = N_, R = R_, MAXR = MAXR_;
-  static constexpr int TPL = N / R;                      // threads per line
-  static constexpr int LG = TPL >= 32 ? 1 : 32 / TPL;    // lines per group
-  static constexpr int GT = TPL * LG;                    // threads per group
-  static constexpr int GW = GT / 32;                     // warps per group
-  static constexpr int GPC = GW >= 4 ? 1 : 4 / GW;       // groups per CTA
-  static constexpr int NT = GPC * GT;                    // threads per CTA
+  static constexpr int TPL = N / R;                                     // threads per line
+  static constexpr int LG = TPL <= 8 ? 32 / TPL : (TPL <= 32 ? 4 : 1);  // lines per group
+  static constexpr int GT = TPL * LG;                                   // threads per group
+  static constexpr int GW = GT / 32;                                    // warps per group
+  static constexpr int NSL = LastNS<N, R>::value;                       // the last pass starts at sub-size NSL
+  static constexpr int RSL = Pass<N, R, NSL>::RS;                       // ... with radix RSL
+  static constexpr int NB = R / 2 + 1;                                  // bins per thread (R/2 + Nyquist slot)
+  static constexpr int NBINS = N / 2 + 1;
   // Register budget (32-bit registers): a thread holds x (4R), its persistent input state (the
   // coefficients a, or the inverse's input-bin values: 2R resp. 2 NB MAXR) and its output accumulators
   // (the forward's bin rows y: 2 NB MAXR, or the inverse's acc: 2R).  For R >= 32 that exceeds 255, so
-  // the input state lives in a thread-private SMEM area (PRIV), read once per term (8 B per point).
+  // the input state lives in a thread-private SMEM area (PRIV), read once per term (8 B per point), and
+  // the exchange runs one real plane at a time (SPLITX) to leave SMEM for the factor ring.
   static constexpr bool PRIV = R >= 32;
+  static constexpr bool SPLITX = R >= 32;
+  static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
   static constexpr int REGS = R >= 32 ? 255 : (MAXR > 2 ? 200 : 168);
-  static constexpr int MINB = 65536 / (REGS * NT) > 0 ? 65536 / (REGS * NT) : 1;  // CTAs per SM
-  static constexpr int NSL = LastNS<N, R>::value;        // the last pass starts at sub-size NSL
-  static constexpr int RSL = Pass<N, R, NSL>::RS;        // ... with radix RSL
-  static constexpr int NB = R / 2 + 1;                   // bins per thread (R/2 + the Nyquist slot)
-  // exchange buffer: double2 slots [pos][line], LG pad slots after every R positions -> the strided
-  // first-pass stores and the unit-stride loads are both free of bank conflicts
+  // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
+  // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;
   static constexpr int PSLOTS = PRIV ? (R > NB * MAXR ? R : NB * MAXR) : 0;  // private doubles per thread
-  static constexpr int GROUP_BYTES = SLOTS * 16 + K0MAX * LG * 8 + PSLOTS * GT * 8;
-  static constexpr size_t smem_bytes() { return (size_t)GPC * GROUP_BYTES; }
+  static constexpr int GROUP_BYTES = ((SLOTS * XB + K0MAX * LG * 8 + PSLOTS * GT * 8) + 127) / 128 * 128;
+  // factor ring: stage = v_l (N complex) + u~_l (MAXR x NBINS complex)
+  static constexpr bool STAGED = N <= 1024;
+  static constexpr int NSTAGE = 2;
+  static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16;
+  static constexpr int STAGE_BYTES = STAGED ? (V_BYTES + U_BYTES + 127) / 128 * 128 : 0;
+  static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
+  static constexpr int gpc_fit(int g) {
+    return (g > 1 && (((g * GT + 127) / 128) * 128 * REGS > 65536 || g * GROUP_BYTES + RING_BYTES + 256 > SMEM_LIMIT || g * GW > 15 ||
+                      g * GT > 1024))
+               ? gpc_fit(g - 1)
+               : g;
+  }
+  static constexpr int GPC = gpc_fit(8);  // groups per CTA (one CTA per SM)
+  static constexpr int NT = GPC * GT;      // threads per CTA
+  static constexpr size_t smem_bytes() { return (size_t)RING_BYTES + 256 + (size_t)GPC * GROUP_BYTES; }
   __device__ static __forceinline__ int sidx(int pos, int line) { return (pos + pos / R) * LG + line; }
   static_assert(GT % 32 == 0, "group must be whole warps");
   static_assert(RSL >= 2, "last pass radix");
@@ -115,28 +136,106 @@ __device__ __forceinline__ void group_sync() {
   if constexpr (C::GW == 1) {
     __syncwarp();
   } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / C::GT)), "r"(C::GT) : "memory");
+    // non-.aligned form: correct even if a warp arrives diverged (PTX ISA, barrier.sync)
+    asm volatile("barrier.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / C::GT)), "r"(C::GT) : "memory");
   }
 }
 
+// ---- mbarrier / TMA bulk-copy helpers (PTX ISA: mbarrier, cp.async.bulk) ---------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra WAIT;\n"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// The CTA's factor ring.  Sequence number seq = (batch iteration) r + l walks the terms of every batch
+// the CTA processes; term seq lives in stage seq % NSTAGE, phase (seq / NSTAGE) & 1.
+template <class C>
+struct Ring {
+  char *base;
+  uint64_t *full, *empty;
+  long long total;  // terms this CTA will consume
+  const double2 *gv, *gu;
+  int r;
+  __device__ __forceinline__ double2 *v(long long seq) const {
+    return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES);
+  }
+  __device__ __forceinline__ double2 *u(long long seq) const {
+    return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::V_BYTES);
+  }
+  __device__ __forceinline__ void issue(long long seq) const {  // producer: one thread
+    const int s = (int)(seq % C::NSTAGE);
+    const int l = (int)(seq % r);
+    mbar_arrive_expect_tx(&full[s], C::V_BYTES + C::U_BYTES);
+    tma_load_1d(v(seq), gv + (long long)l * C::N, C::V_BYTES, &full[s]);
+    tma_load_1d(u(seq), gu + (long long)l * C::MAXR * C::NBINS, C::U_BYTES, &full[s]);
+  }
+  __device__ __forceinline__ void wait_full(long long seq) const {
+    mbar_wait(&full[seq % C::NSTAGE], (uint32_t)((seq / C::NSTAGE) & 1));
+    __syncwarp();  // lanes may leave the try_wait loop in different iterations: reconverge
+  }
+  // called by every thread of every group after its end-of-term group_sync
+  __device__ __forceinline__ void release(long long seq, int gt) const {
+    if (gt == 0) mbar_arrive(&empty[seq % C::NSTAGE]);
+    if (threadIdx.x == 0 && seq + C::NSTAGE < total) {
+      mbar_wait(&empty[seq % C::NSTAGE], (uint32_t)((seq / C::NSTAGE) & 1));
+      issue(seq + C::NSTAGE);
+    }
+    // reconverge warp 0 before the group's next (warp-aligned) bar.sync: bar.sync from a diverged warp
+    // is undefined and released the barrier early (a race seen on 512^3 axis-0 lines)
+    __syncwarp();
+  }
+};
+
 // ---- Stockham passes over the group's exchange buffer -------------------------------------------------
 
+// Store one real plane (SPLITX) or both (interleaved double2) of the outputs of the pass at sub-size NS.
 template <class C, int NS>
-__device__ __forceinline__ void pass_store(const double (&xr)[C::R], const double (&xi)[C::R], double2 *buf, int vt,
-                                           int line) {
+__device__ __forceinline__ void pass_store(const double (&xr)[C::R], const double (&xi)[C::R], void *buf, int vt,
+                                           int line, int plane) {
   using P = Pass<C::N, C::R, NS>;
 #pragma unroll
   for (int i = 0; i < P::B; ++i) {
     const int v = vt + i * C::TPL;
     const int idxD = (v / NS) * NS * P::RS + (v % NS);
 #pragma unroll
-    for (int s = 0; s < P::RS; ++s) buf[C::sidx(idxD + s * NS, line)] = make_double2(xr[i * P::RS + s], xi[i * P::RS + s]);
+    for (int s = 0; s < P::RS; ++s) {
+      const int sl = C::sidx(idxD + s * NS, line);
+      if constexpr (C::SPLITX) {
+        static_cast<double *>(buf)[sl] = plane == 0 ? xr[i * P::RS + s] : xi[i * P::RS + s];
+      } else {
+        static_cast<double2 *>(buf)[sl] = make_double2(xr[i * P::RS + s], xi[i * P::RS + s]);
+      }
+    }
   }
 }
 
+// Load the inputs of the pass at sub-size NS (one plane, or both).
 template <class C, int NS>
-__device__ __forceinline__ void pass_load_compute(double (&xr)[C::R], double (&xi)[C::R], const double2 *buf, int vt,
-                                                  int line, const double2 *__restrict__ tw) {
+__device__ __forceinline__ void pass_load(double (&xr)[C::R], double (&xi)[C::R], const void *buf, int vt, int line,
+                                          int plane) {
   using P = Pass<C::N, C::R, NS>;
   constexpr int RS = P::RS;
 #pragma unroll
@@ -144,31 +243,81 @@ __device__ __forceinline__ void pass_load_compute(double (&xr)[C::R], double (&x
     const int v = vt + i * C::TPL;
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
-      const double2 d = buf[C::sidx(v + r * (C::N / RS), line)];
-      xr[i * RS + r] = d.x;
-      xi[i * RS + r] = d.y;
+      const int sl = C::sidx(v + r * (C::N / RS), line);
+      if constexpr (C::SPLITX) {
+        if (plane == 0) xr[i * RS + r] = static_cast<const double *>(buf)[sl];
+        else xi[i * RS + r] = static_cast<const double *>(buf)[sl];
+      } else {
+        const double2 d = static_cast<const double2 *>(buf)[sl];
+        xr[i * RS + r] = d.x;
+        xi[i * RS + r] = d.y;
+      }
     }
+  }
+}
+
+// Twiddle and radix-RS butterflies of the pass at sub-size NS (inputs already in registers).
+template <class C, int NS>
+__device__ __forceinline__ void pass_compute(double (&xr)[C::R], double (&xi)[C::R], int vt,
+                                             const double2 *__restrict__ tw) {
+  using P = Pass<C::N, C::R, NS>;
+  constexpr int RS = P::RS;
+#pragma unroll
+  for (int i = 0; i < P::B; ++i) {
+    const int v = vt + i * C::TPL;
+    // Twiddles w^r, w = e^{2 pi i (v mod NS) / (NS RS)}: exact table values at the anchors r = 1 (mod 8),
+    // the rest by the chain w^r = w^{r-1} w (<= 7 roundings from an anchor).  A load costs the L1 data
+    // pipe 4 cycles per warp (tools/l1_probe.cu) while a complex multiply costs the FP64 pipe 2.
     const double2 *twp = tw + TwOff<C::N, C::R, NS>::value + (v % NS);
+    const double2 w1 = __ldg(&twp[0]);
+    double pr = 1.0, pim = 0.0;
 #pragma unroll
     for (int r = 1; r < RS; ++r) {
-      const double2 w = __ldg(&twp[(r - 1) * NS]);
-      const double tr = xr[i * RS + r] * w.x - xi[i * RS + r] * w.y;
-      xi[i * RS + r] = fma(xr[i * RS + r], w.y, xi[i * RS + r] * w.x);
+      if (r % 8 == 1) {
+        const double2 wa = r == 1 ? w1 : __ldg(&twp[(r - 1) * NS]);
+        pr = wa.x;
+        pim = wa.y;
+      } else {
+        const double t = pr * w1.x - pim * w1.y;
+        pim = fma(pr, w1.y, pim * w1.x);
+        pr = t;
+      }
+      const double tr = xr[i * RS + r] * pr - xi[i * RS + r] * pim;
+      xi[i * RS + r] = fma(xr[i * RS + r], pim, xi[i * RS + r] * pr);
       xr[i * RS + r] = tr;
     }
     dft<RS>(&xr[i * RS], &xi[i * RS]);
   }
 }
 
+// Exchange the outputs of the pass that started at NSS (in registers) into the inputs of the pass at
+// NS = NSS RS(NSS).  On entry every thread of the group has finished reading the buffer.
+template <class C, int NSS>
+__device__ __forceinline__ void do_exchange(double (&xr)[C::R], double (&xi)[C::R], void *buf, int vt, int line) {
+  constexpr int NS = NSS * Pass<C::N, C::R, NSS>::RS;
+  if constexpr (C::SPLITX) {
+    pass_store<C, NSS>(xr, xi, buf, vt, line, 0);
+    group_sync<C>();
+    pass_load<C, NS>(xr, xi, buf, vt, line, 0);
+    group_sync<C>();
+    pass_store<C, NSS>(xr, xi, buf, vt, line, 1);
+    group_sync<C>();
+    pass_load<C, NS>(xr, xi, buf, vt, line, 1);
+  } else {
+    pass_store<C, NSS>(xr, xi, buf, vt, line, 0);
+    group_sync<C>();
+    pass_load<C, NS>(xr, xi, buf, vt, line, 0);
+  }
+}
+
 template <class C, int NS>
-__device__ __forceinline__ void run_passes(double (&xr)[C::R], double (&xi)[C::R], double2 *buf, int vt, int line,
+__device__ __forceinline__ void run_passes(double (&xr)[C::R], double (&xi)[C::R], void *buf, int vt, int line,
                                            const double2 *__restrict__ tw) {
   if constexpr (NS < C::N) {
-    pass_load_compute<C, NS>(xr, xi, buf, vt, line, tw);
+    pass_compute<C, NS>(xr, xi, vt, tw);
     if constexpr (!Pass<C::N, C::R, NS>::LAST) {
       group_sync<C>();
-      pass_store<C, NS>(xr, xi, buf, vt, line);
-      group_sync<C>();
+      do_exchange<C, NS>(xr, xi, buf, vt, line);
       run_passes<C, NS * Pass<C::N, C::R, NS>::RS>(xr, xi, buf, vt, line, tw);
     }
   }
@@ -177,14 +326,13 @@ __device__ __forceinline__ void run_passes(double (&xr)[C::R], double (&xi)[C::R
 // Full FFT of one term; first-pass inputs (positions vt + r TPL) in registers on entry, last-pass
 // outputs (positions out_pos) in registers on exit.  The caller syncs the group before the next call.
 template <class C>
-__device__ __forceinline__ void fft(double (&xr)[C::R], double (&xi)[C::R], double2 *buf, int vt, int line,
+__device__ __forceinline__ void fft(double (&xr)[C::R], double (&xi)[C::R], void *buf, int vt, int line,
                                     const double2 *__restrict__ tw) {
   using P0 = Pass<C::N, C::R, 1>;
 #pragma unroll
   for (int i = 0; i < P0::B; ++i) dft<P0::RS>(&xr[i * P0::RS], &xi[i * P0::RS]);
   if constexpr (!P0::LAST) {
-    pass_store<C, 1>(xr, xi, buf, vt, line);
-    group_sync<C>();
+    do_exchange<C, 1>(xr, xi, buf, vt, line);
     run_passes<C, P0::RS>(xr, xi, buf, vt, line, tw);
   }
 }
@@ -202,29 +350,64 @@ __device__ __forceinline__ constexpr int fwd_reg_of_bin(int q) {
   return q < C::R / 2 ? (q / (C::RSL / 2)) * C::RSL + (q % (C::RSL / 2)) : C::RSL / 2;
 }
 
-// Group geometry shared by both kernels.
+// Per-CTA shared-memory carve-up and per-thread group geometry.
 template <class C>
-struct GroupCtx {
-  int grp, line, vt;
-  long long L, base;
-  bool live;
-  double2 *buf;
-  double *alow;
-  double *priv;  // thread-private slots [slot][gt] (C::PRIV)
-  int gt;
-  __device__ __forceinline__ GroupCtx(double2 *smem, long long nlines, long long inner, int n) {
+struct Ctx {
+  int grp, gt, line, vt;
+  void *buf;     // group exchange buffer
+  double *alow;  // group: k0 x LG low-degree coefficients (forward) / reduced a_V (inverse)
+  double *priv;  // group: thread-private slots [slot][gt] (C::PRIV)
+  Ring<C> ring;
+  long long nbatch;
+  const double2 *gv, *gu;
+  __device__ __forceinline__ Ctx(char *smem, const AxisDev &ax, long long nlines) {
     grp = threadIdx.x / C::GT;
     gt = threadIdx.x % C::GT;
     line = gt % C::LG;
     vt = gt / C::LG;
-    L = ((long long)blockIdx.x * C::GPC + grp) * C::LG + line;
-    live = L < nlines;
-    const long long o = L / inner, i = L - o * inner;
-    base = o * (long long)n * inner + i;
-    char *gb = reinterpret_cast<char *>(smem) + grp * C::GROUP_BYTES;
-    buf = reinterpret_cast<double2 *>(gb);
-    alow = reinterpret_cast<double *>(gb + C::SLOTS * sizeof(double2));
+    gv = ax.v;
+    gu = ax.ub;
+    ring.base = smem;
+    ring.full = reinterpret_cast<uint64_t *>(smem + C::NSTAGE * C::STAGE_BYTES);
+    ring.empty = ring.full + C::NSTAGE;
+    ring.gv = ax.v;
+    ring.gu = ax.ub;
+    ring.r = ax.r;
+    char *gb = smem + ((C::RING_BYTES + 127) / 128) * 128 + grp * C::GROUP_BYTES;
+    buf = gb;
+    alow = reinterpret_cast<double *>(gb + C::SLOTS * C::XB);
     priv = alow + K0MAX * C::LG;
+    nbatch = (nlines + C::GPC * C::LG - 1) / (C::GPC * C::LG);
+    const long long mine = blockIdx.x < nbatch ? (nbatch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    ring.total = mine * ax.r;
+  }
+  // Ring set-up: barriers initialised and the first NSTAGE terms in flight before anyone waits.
+  __device__ __forceinline__ void start() {
+    if constexpr (C::STAGED) {
+      if (threadIdx.x == 0) {
+        for (int s = 0; s < C::NSTAGE; ++s) {
+          mbar_init(&ring.full[s], 1);
+          mbar_init(&ring.empty[s], C::GPC);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (long long q = 0; q < C::NSTAGE && q < ring.total; ++q) ring.issue(q);
+      }
+      __syncthreads();
+    }
+  }
+  __device__ __forceinline__ const double2 *vfac(long long seq, int l) const {
+    if constexpr (C::STAGED) return ring.v(seq);
+    else return gv + (long long)l * C::N;
+  }
+  __device__ __forceinline__ const double2 *ufac(long long seq, int l) const {
+    if constexpr (C::STAGED) return ring.u(seq);
+    else return gu + (long long)l * C::MAXR * C::NBINS;
+  }
+  __device__ __forceinline__ void acquire(long long seq) const {
+    if constexpr (C::STAGED) ring.wait_full(seq);
+  }
+  __device__ __forceinline__ void release(long long seq) const {
+    if constexpr (C::STAGED) ring.release(seq, gt);
   }
 };
 
@@ -247,100 +430,108 @@ struct State {
 };
 
 template <int MAXR>
-__device__ __forceinline__ void load_rows(const double *__restrict__ p, double (&o)[MAXR]) {
-  if constexpr (MAXR % 2 == 0) {
+__device__ __forceinline__ void load_rows(const double *__restrict__ p, int stride, double (&o)[MAXR]) {
 #pragma unroll
-    for (int c = 0; c < MAXR; c += 2) {
-      const double2 t = __ldg(reinterpret_cast<const double2 *>(p + c));
-      o[c] = t.x;
-      o[c + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < MAXR; ++c) o[c] = __ldg(p + c);
-  }
+  for (int c = 0; c < MAXR; ++c) o[c] = __ldg(p + c * stride);
+}
+
+// Global base offset of line L (lines are (outer, inner) pairs, inner fastest; the axis has stride inner).
+__device__ __forceinline__ long long line_base(long long L, long long inner, int n) {
+  const long long o = L / inner, i = L - o * inner;
+  return o * (long long)n * inner + i;
 }
 
 // ------------------------------------------------------------------------------------------------
 // Forward axis pass (K4).
 // ------------------------------------------------------------------------------------------------
 template <class C>
-__global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, const double *in, double *out, long long nlines,
-                                                          long long inner) {
-  constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR;
-  extern __shared__ double2 smem[];
-  GroupCtx<C> g(smem, nlines, inner, ax.n);
-  const int n = ax.n, k0 = ax.k0, nbins = ax.nbins;
-  const int vt = g.vt, line = g.line;
-
-  // coefficients at the first-pass input positions k = vt + r TPL
-  State<C, R> a(g.priv, g.gt);
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int k = vt + r * TPL;
-    const double ak = (g.live && k < n) ? in[g.base + (long long)k * inner] : 0.0;
-    a.set(r, ak);
-    if (r * TPL < K0MAX && k < k0) g.alow[k * LG + line] = ak;
-  }
+__global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
+                                                             long long nlines, long long inner) {
+  constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
+  extern __shared__ __align__(128) char smem_raw[];
+  Ctx<C> cx(smem_raw, ax, nlines);
+  cx.start();
+  const int n = ax.n, k0 = ax.k0;
+  const int vt = cx.vt, line = cx.line;
 
   int m[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) m[q] = q < R / 2 ? out_pos<C>(vt, fwd_reg_of_bin<C>(q)) : C::N / 2;
 
-  // A4: y = W V a_V on the rows of the thread's bins
-  double y[NB][MAXR];
-#pragma unroll
-  for (int q = 0; q < NB; ++q)
-#pragma unroll
-    for (int c = 0; c < MAXR; ++c) y[q][c] = 0.0;
-  group_sync<C>();
-  for (int k = 0; k < k0; ++k) {
-    const double ak = g.alow[k * LG + line];
-    const double *pk = ax.phivb + (long long)k * nbins * MAXR;
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      double pv[MAXR];
-      load_rows<MAXR>(pk + m[q] * MAXR, pv);
-#pragma unroll
-      for (int c = 0; c < MAXR; ++c) y[q][c] = fma(pv[c], ak, y[q][c]);
-    }
-  }
+  long long seq = 0;
+  for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
+    const long long L = (bt * C::GPC + cx.grp) * LG + line;
+    const bool live = L < nlines;
+    const long long base = line_base(live ? L : 0, inner, n);
 
-  for (int l = 0; l < ax.r; ++l) {
-    const double2 *vl = ax.v + (long long)l * C::N;
-    const double2 *ul = ax.ub + (long long)l * nbins * MAXR;
-    double xr[R], xi[R];
+    // coefficients at the first-pass input positions k = vt + r TPL; degrees < k0 also to alow
+    State<C, R> a(cx.priv, cx.gt);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {  // A1
-      const double2 vv = __ldg(&vl[vt + r * TPL]);
-      const double ar = a.get(r);
-      xr[r] = vv.x * ar;
-      xi[r] = vv.y * ar;
+    for (int r = 0; r < R; ++r) {
+      const int k = vt + r * TPL;
+      const double ak = (live && k < n) ? in[base + (long long)k * inner] : 0.0;
+      a.set(r, ak);
+      if (r * TPL < K0MAX && k < k0) cx.alow[k * LG + line] = ak;
     }
-    fft<C>(xr, xi, g.buf, vt, line, ax.tw + (l >> 30));  // A2 (see Cfg::REGS)
+
+    // A4: y = W V a_V on the rows of the thread's bins
+    double y[NB][MAXR];
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {  // A3
-      const int e = fwd_reg_of_bin<C>(q);
+    for (int q = 0; q < NB; ++q)
 #pragma unroll
-      for (int c = 0; c < MAXR; ++c) {
-        const double2 uu = __ldg(&ul[m[q] * MAXR + c]);
-        y[q][c] = fma(uu.x, xr[e], y[q][c]);
-        y[q][c] = fma(-uu.y, xi[e], y[q][c]);
+      for (int c = 0; c < MAXR; ++c) y[q][c] = 0.0;
+    group_sync<C>();
+    for (int k = 0; k < k0; ++k) {
+      const double ak = cx.alow[k * LG + line];
+      const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        double pv[MAXR];
+        load_rows<MAXR>(pk + m[q], NBINS, pv);
+#pragma unroll
+        for (int c = 0; c < MAXR; ++c) y[q][c] = fma(pv[c], ak, y[q][c]);
       }
     }
-    group_sync<C>();  // the next term's first store overwrites the exchange buffer
-  }
 
-  if (g.live) {
+    for (int l = 0; l < ax.r; ++l, ++seq) {
+      cx.acquire(seq);
+      const double2 *vl = cx.vfac(seq, l);
+      const double2 *ul = cx.ufac(seq, l);
+      double xr[R], xi[R];
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      if (q < R / 2 || vt == 0) {
-        const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
+      for (int r = 0; r < R; ++r) {  // A1
+        const double2 vv = vl[vt + r * TPL];
+        const double ar = a.get(r);
+        xr[r] = vv.x * ar;
+        xi[r] = vv.y * ar;
+      }
+      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30));  // A2 (opaque offset: no hoisting of twiddles)
 #pragma unroll
-        for (int c = 0; c < MAXR; ++c)
-          if (c < cnt) out[g.base + (long long)(j0 + c) * inner] = y[q][c];
+      for (int q = 0; q < NB; ++q) {  // A3
+        const int e = fwd_reg_of_bin<C>(q);
+#pragma unroll
+        for (int c = 0; c < MAXR; ++c) {
+          const double2 uu = ul[c * NBINS + m[q]];
+          y[q][c] = fma(uu.x, xr[e], y[q][c]);
+          y[q][c] = fma(-uu.y, xi[e], y[q][c]);
+        }
+      }
+      group_sync<C>();  // exchange buffer and this stage are free again
+      cx.release(seq);
+    }
+
+    if (live) {
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        if (q < R / 2 || vt == 0) {
+          const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
+#pragma unroll
+          for (int c = 0; c < MAXR; ++c)
+            if (c < cnt) out[base + (long long)(j0 + c) * inner] = y[q][c];
+        }
       }
     }
+    group_sync<C>();  // alow / PRIV reuse by the next batch
   }
 }
 
@@ -348,99 +539,118 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
 // Inverse axis pass (K5).
 // ------------------------------------------------------------------------------------------------
 template <class C>
-__global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, const double *in, double *out, long long nlines,
-                                                          long long inner) {
-  constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR;
-  extern __shared__ double2 smem[];
-  GroupCtx<C> g(smem, nlines, inner, ax.n);
-  const int n = ax.n, k0 = ax.k0, nbins = ax.nbins;
-  const int vt = g.vt, line = g.line;
+__global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const double *in, double *out,
+                                                             long long nlines, long long inner) {
+  constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
+  extern __shared__ __align__(128) char smem_raw[];
+  Ctx<C> cx(smem_raw, ax, nlines);
+  cx.start();
+  const int n = ax.n, k0 = ax.k0;
+  const int vt = cx.vt, line = cx.line;
 
   // input bins: q < R/2 -> first-pass position vt + q TPL; q = R/2 -> position vt + N/2 (Nyquist, vt == 0)
   int m[NB];
-  State<C, NB * MAXR> yb(g.priv, g.gt);  // yb(q MAXR + c): row c of input bin q
 #pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    const bool own = q < R / 2 || vt == 0;
-    m[q] = q < R / 2 ? vt + q * TPL : C::N / 2;
-    const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
-#pragma unroll
-    for (int c = 0; c < MAXR; ++c)
-      yb.set(q * MAXR + c, (g.live && own && c < cnt) ? in[g.base + (long long)(j0 + c) * inner] : 0.0);
-  }
+  for (int q = 0; q < NB; ++q) m[q] = q < R / 2 ? vt + q * TPL : C::N / 2;
 
-  // a_V = (W V)^T y: thread partial sums over its rows, reduced over the TPL threads of the line
-  for (int k = 0; k < k0; ++k) {
-    const double *pk = ax.phivb + (long long)k * nbins * MAXR;
-    double p = 0.0;
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      double pv[MAXR];
-      load_rows<MAXR>(pk + m[q] * MAXR, pv);
-#pragma unroll
-      for (int c = 0; c < MAXR; ++c) p = fma(pv[c], yb.get(q * MAXR + c), p);
-    }
-    if constexpr (C::GW == 1) {
-#pragma unroll
-      for (int off = LG; off < 32; off *= 2) p += __shfl_xor_sync(0xffffffffu, p, off);
-      if (vt == 0) g.alow[k * LG + line] = p;
-    } else {
-#pragma unroll
-      for (int off = 1; off < 32; off *= 2) p += __shfl_xor_sync(0xffffffffu, p, off);
-      if ((threadIdx.x & 31) == 0) reinterpret_cast<double *>(g.buf)[k * C::GW + vt / 32] = p;
-    }
-  }
-  if constexpr (C::GW > 1) {
-    group_sync<C>();
-    if (vt < k0) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < C::GW; ++w) s += reinterpret_cast<double *>(g.buf)[vt * C::GW + w];
-      g.alow[vt] = s;
-    }
-  }
-  group_sync<C>();
+  long long seq = 0;
+  for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
+    const long long L = (bt * C::GPC + cx.grp) * LG + line;
+    const bool live = L < nlines;
+    const long long base = line_base(live ? L : 0, inner, n);
 
-  double acc[R];
+    State<C, NB * MAXR> yb(cx.priv, cx.gt);  // yb(q MAXR + c): row c of input bin q
+    {
+      // a_V = (W V)^T y: thread partial sums over its rows (held in registers here: nothing else is
+      // live yet), reduced over the TPL threads of the line (shuffles within the warp, then SMEM across
+      // the GW warps of a multi-warp group)
+      double yr[NB * MAXR];
 #pragma unroll
-  for (int e = 0; e < R; ++e) acc[e] = 0.0;
-
-  for (int l = 0; l < ax.r; ++l) {
-    const double2 *vl = ax.v + (long long)l * C::N;
-    const double2 *ul = ax.ub + (long long)l * nbins * MAXR;
-    double xr[R], xi[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      xr[r] = 0.0;
-      xi[r] = 0.0;
-      if (r <= R / 2) {  // bin sums (positions > N/2 hold no rows)
+      for (int q = 0; q < NB; ++q) {
+        const bool own = q < R / 2 || vt == 0;
+        const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
 #pragma unroll
         for (int c = 0; c < MAXR; ++c) {
-          const double2 uu = __ldg(&ul[m[r] * MAXR + c]);
-          const double yv = yb.get(r * MAXR + c);
-          xr[r] = fma(uu.x, yv, xr[r]);
-          xi[r] = fma(uu.y, yv, xi[r]);
+          yr[q * MAXR + c] = (live && own && c < cnt) ? in[base + (long long)(j0 + c) * inner] : 0.0;
+          yb.set(q * MAXR + c, yr[q * MAXR + c]);
         }
       }
-    }
-    fft<C>(xr, xi, g.buf, vt, line, ax.tw + (l >> 30));
+      double *red = static_cast<double *>(cx.buf);  // k0 x GW x LG partials (exchange buffer is free)
+      for (int k = 0; k < k0; ++k) {
+        const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
+        double p = 0.0;
 #pragma unroll
-    for (int e = 0; e < R; ++e) {  // a[k] += Re(v_l[k] B[k])
-      const double2 vv = __ldg(&vl[out_pos<C>(vt, e)]);
-      acc[e] = fma(vv.x, xr[e], acc[e]);
-      acc[e] = fma(-vv.y, xi[e], acc[e]);
+        for (int q = 0; q < NB; ++q) {
+          double pv[MAXR];
+          load_rows<MAXR>(pk + m[q], NBINS, pv);
+#pragma unroll
+          for (int c = 0; c < MAXR; ++c) p = fma(pv[c], yr[q * MAXR + c], p);
+        }
+#pragma unroll
+        for (int off = LG; off < 32; off *= 2) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if constexpr (C::GW == 1) {
+          if (vt == 0) cx.alow[k * LG + line] = p;
+        } else {
+          if ((threadIdx.x & 31) < LG) red[(k * C::GW + (cx.gt >> 5)) * LG + line] = p;
+        }
+      }
+      if constexpr (C::GW > 1) {
+        group_sync<C>();
+        for (int i = cx.gt; i < k0 * LG; i += C::GT) {
+          const int k = i / LG, ln = i % LG;
+          double s = 0.0;
+#pragma unroll
+          for (int w = 0; w < C::GW; ++w) s += red[(k * C::GW + w) * LG + ln];
+          cx.alow[k * LG + ln] = s;
+        }
+      }
+      group_sync<C>();
+    }
+
+    double acc[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) acc[e] = 0.0;
+
+    for (int l = 0; l < ax.r; ++l, ++seq) {
+      cx.acquire(seq);
+      const double2 *vl = cx.vfac(seq, l);
+      const double2 *ul = cx.ufac(seq, l);
+      double xr[R], xi[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        xr[r] = 0.0;
+        xi[r] = 0.0;
+        if (r <= R / 2) {  // bin sums (positions > N/2 hold no rows)
+#pragma unroll
+          for (int c = 0; c < MAXR; ++c) {
+            const double2 uu = ul[c * NBINS + m[r]];
+            const double yv = yb.get(r * MAXR + c);
+            xr[r] = fma(uu.x, yv, xr[r]);
+            xi[r] = fma(uu.y, yv, xi[r]);
+          }
+        }
+      }
+      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30));
+#pragma unroll
+      for (int e = 0; e < R; ++e) {  // a[k] += Re(v_l[k] B[k])
+        const double2 vv = vl[out_pos<C>(vt, e)];
+        acc[e] = fma(vv.x, xr[e], acc[e]);
+        acc[e] = fma(-vv.y, xi[e], acc[e]);
+      }
+      group_sync<C>();
+      cx.release(seq);
+    }
+
+    if (live) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const int k = out_pos<C>(vt, e);
+        double val = acc[e];
+        if (k < k0) val += cx.alow[k * LG + line];
+        if (k < n) out[base + (long long)k * inner] = val;
+      }
     }
     group_sync<C>();
-  }
-
-  if (g.live) {
-#pragma unroll
-    for (int e = 0; e < R; ++e) {
-      const int k = out_pos<C>(vt, e);
-      double val = acc[e];
-      if (k < k0) val += g.alow[k * LG + line];
-      if (k < n) out[g.base + (long long)k * inner] = val;
-    }
   }
 }
 

@@ -92,22 +92,26 @@ constexpr int radix_for() {
 }
 int radix_of(int64_t N, int maxr) { return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : 32))); }
 
+// Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
 template <class C>
 jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
                      long long inner, cudaStream_t s) {
   const size_t smem = C::smem_bytes();
-  const long long lines_per_cta = (long long)C::GPC * C::LG;
-  const long long blocks = (nlines + lines_per_cta - 1) / lines_per_cta;
-  if (blocks == 0) return JT_OK;
-  if (blocks > 0x7fffffffLL) return fail(JT_ERR_ARG, "too many lines for one launch");
+  const long long lines_per_batch = (long long)C::GPC * C::LG;
+  const long long batches = (nlines + lines_per_batch - 1) / lines_per_batch;
+  if (batches == 0) return JT_OK;
+  int dev = 0, sms = 148;
+  JT_CUDA_TRY(cudaGetDevice(&dev));
+  JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid = (unsigned)std::min<long long>(batches, sms);
   if (inverse) {
     auto kern = jtk::inv_axis_kernel<C>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)blocks, C::NT, smem, s>>>(ax, in, out, nlines, inner);
+    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, inner);
   } else {
     auto kern = jtk::fwd_axis_kernel<C>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)blocks, C::NT, smem, s>>>(ax, in, out, nlines, inner);
+    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, inner);
   }
   JT_CUDA_TRY(cudaGetLastError());
   return JT_OK;
@@ -187,9 +191,9 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
       const int64_t j = h.bstart[m] + c;
       for (int l = 0; l < r; ++l) {
         const jt::cd z = h.u[(size_t)j * r + l];
-        ub[((size_t)l * nbins + m) * MAXR + c] = make_double2(z.real(), z.imag());
+        ub[((size_t)l * MAXR + c) * nbins + m] = make_double2(z.real(), z.imag());
       }
-      for (int k = 0; k < k0; ++k) phivb[((size_t)k * nbins + m) * MAXR + c] = h.phiv[(size_t)j * k0 + k];
+      for (int k = 0; k < k0; ++k) phivb[((size_t)k * MAXR + c) * nbins + m] = h.phiv[(size_t)j * k0 + k];
     }
   }
   for (int l = 0; l < r; ++l) {

@@ -121,6 +121,33 @@ def test_full_size_sampled(name):
         assert relerr(got2, ref2) <= TOL
 
 
+def test_cfg5_full_forward_and_determinism():
+    """The bench workload (512^3) compared over the WHOLE array (a sampled check once missed a race that
+    corrupted ~1e-4 of the rows), and bitwise-repeatable forward and inverse (no atomics anywhere)."""
+    c = si.CONFIGS["cfg5_3d_512"]
+    p = jt.Plan(c["n"], c["a"], c["b"], c["eps"])
+    x = si.gaussian(c["n"], seed=0)
+    xd = torch.from_numpy(x).cuda()
+    y1 = torch.empty_like(xd)
+    y2 = torch.empty_like(xd)
+    jt.jt_forward(p.handle, xd, y1)
+    jt.jt_forward(p.handle, xd, y2)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    z1 = torch.empty_like(xd)
+    z2 = torch.empty_like(xd)
+    jt.jt_inverse(p.handle, y1, z1)
+    jt.jt_inverse(p.handle, y1, z2)
+    torch.cuda.synchronize()
+    assert torch.equal(z1, z2)
+    y = y1.cpu().numpy()
+    del y1, y2, z2
+    ref = oracle.forward(x, c["a"], c["b"])
+    assert relerr(y, ref) <= TOL
+    assert np.max(np.abs(y - ref)) <= 1e-10 * np.max(np.abs(ref))
+    assert relerr(z1.cpu().numpy(), x) <= TOL
+
+
 def test_inplace_and_stream_and_determinism():
     shape, a, b = (96, 200), (0.3, -0.1), (0.2, 0.4)
     p = jt.Plan(shape, a, b, 1e-12)
