@@ -95,6 +95,18 @@ jt_status jt_forward_axis(jt_plan_t p, int axis, const double *in, double *out, 
 jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer,
                           int64_t inner, void *cuda_stream);
 
+/* General axis pass, the building block of the slab-distributed schedule (the paper's
+ * "n 2D transforms and n^2 1D transforms", with the transpose between them).  Applies axis
+ * `axis`'s 1D forward (inverse != 0: inverse) transform to every line of an (outer, n[axis], inner)
+ * device array.  in_split / out_split = G >= 1 (G | n[axis]) select the CHUNK-MAJOR layout of the input /
+ * output: with c = n[axis] / G, element j of line (o, i) is at
+ *     (j / c) * (outer * c * inner) + o * c * inner + (j % c) * inner + i
+ * (G = 1: plain C-order).  Chunk g is then the contiguous block an all-to-all sends to / receives from
+ * rank g, so no pack or unpack kernel exists.  Chunk-major layouts need in != out (else JT_ERR_ARG); with
+ * both splits 1, in == out is allowed. */
+jt_status jt_axis_pass(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
+                       int64_t inner, int in_split, int out_split, void *cuda_stream);
+
 /* Free a plan (device buffers included).  jt_destroy(NULL) is JT_OK. */
 jt_status jt_destroy(jt_plan_t p);
 

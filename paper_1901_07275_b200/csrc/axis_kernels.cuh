@@ -435,18 +435,39 @@ __device__ __forceinline__ void load_rows(const double *__restrict__ p, int stri
   for (int c = 0; c < MAXR; ++c) o[c] = __ldg(p + c * stride);
 }
 
-// Global base offset of line L (lines are (outer, inner) pairs, inner fastest; the axis has stride inner).
-__device__ __forceinline__ long long line_base(long long L, long long inner, int n) {
-  const long long o = L / inner, i = L - o * inner;
-  return o * (long long)n * inner + i;
-}
+// Addressing of one line's elements.  Lines are (outer, inner) pairs, inner fastest; element j of line
+// (o, i) of an axis of length n lives at o n inner + j inner + i (plain C-order), or, in the CHUNK-MAJOR
+// layout of the slab all-to-all (cs = n / G chunk length),
+//     (j / cs) (outer cs inner) + o cs inner + (j % cs) inner + i,
+// which for cs == n is the plain layout.  The layout flag is uniform per launch.
+struct Layout {
+  long long outer, inner;
+  int in_cs, out_cs;  // chunk length of the input / output along the axis (== n: plain C-order)
+};
+
+struct LineAddr {
+  long long b0, cstride, inner;
+  int cs;
+  bool plain;
+  __device__ __forceinline__ LineAddr(long long L, long long outer, long long inner_, int n, int cs_) {
+    const long long o = L / inner_, i = L - o * inner_;
+    inner = inner_;
+    cs = cs_;
+    plain = cs_ == n;
+    b0 = o * (long long)cs_ * inner_ + i;
+    cstride = outer * (long long)cs_ * inner_;
+  }
+  __device__ __forceinline__ long long at(int j) const {
+    return plain ? b0 + (long long)j * inner : b0 + (long long)(j / cs) * cstride + (long long)(j % cs) * inner;
+  }
+};
 
 // ------------------------------------------------------------------------------------------------
 // Forward axis pass (K4).
 // ------------------------------------------------------------------------------------------------
 template <class C>
 __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, long long inner) {
+                                                             long long nlines, Layout lay) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C> cx(smem_raw, ax, nlines);
@@ -462,14 +483,15 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const long long base = line_base(live ? L : 0, inner, n);
+    const LineAddr ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
+    const LineAddr oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
 
     // coefficients at the first-pass input positions k = vt + r TPL; degrees < k0 also to alow
     State<C, R> a(cx.priv, cx.gt);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int k = vt + r * TPL;
-      const double ak = (live && k < n) ? in[base + (long long)k * inner] : 0.0;
+      const double ak = (live && k < n) ? in[ia.at(k)] : 0.0;
       a.set(r, ak);
       if (r * TPL < K0MAX && k < k0) cx.alow[k * LG + line] = ak;
     }
@@ -527,7 +549,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
           const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
 #pragma unroll
           for (int c = 0; c < MAXR; ++c)
-            if (c < cnt) out[base + (long long)(j0 + c) * inner] = y[q][c];
+            if (c < cnt) out[oa.at(j0 + c)] = y[q][c];
         }
       }
     }
@@ -540,7 +562,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 // ------------------------------------------------------------------------------------------------
 template <class C>
 __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, long long inner) {
+                                                             long long nlines, Layout lay) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C> cx(smem_raw, ax, nlines);
@@ -557,7 +579,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const long long base = line_base(live ? L : 0, inner, n);
+    const LineAddr ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
+    const LineAddr oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
 
     State<C, NB * MAXR> yb(cx.priv, cx.gt);  // yb(q MAXR + c): row c of input bin q
     {
@@ -571,7 +594,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
 #pragma unroll
         for (int c = 0; c < MAXR; ++c) {
-          yr[q * MAXR + c] = (live && own && c < cnt) ? in[base + (long long)(j0 + c) * inner] : 0.0;
+          yr[q * MAXR + c] = (live && own && c < cnt) ? in[ia.at(j0 + c)] : 0.0;
           yb.set(q * MAXR + c, yr[q * MAXR + c]);
         }
       }
@@ -647,7 +670,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         const int k = out_pos<C>(vt, e);
         double val = acc[e];
         if (k < k0) val += cx.alow[k * LG + line];
-        if (k < n) out[base + (long long)k * inner] = val;
+        if (k < n) out[oa.at(k)] = val;
       }
     }
     group_sync<C>();

@@ -95,7 +95,7 @@ int radix_of(int64_t N, int maxr) { return maxr > 2 ? 16 : (N == 16 ? 16 : (N ==
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
 template <class C>
 jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                     long long inner, cudaStream_t s) {
+                     const jtk::Layout &lay, cudaStream_t s) {
   const size_t smem = C::smem_bytes();
   const long long lines_per_batch = (long long)C::GPC * C::LG;
   const long long batches = (nlines + lines_per_batch - 1) / lines_per_batch;
@@ -107,11 +107,11 @@ jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, dou
   if (inverse) {
     auto kern = jtk::inv_axis_kernel<C>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, inner);
+    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay);
   } else {
     auto kern = jtk::fwd_axis_kernel<C>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, inner);
+    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay);
   }
   JT_CUDA_TRY(cudaGetLastError());
   return JT_OK;
@@ -119,26 +119,29 @@ jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, dou
 
 template <int N>
 jt_status launch_n(bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                   long long inner, cudaStream_t s) {
-  if (maxr <= 2) return launch_cfg<jtk::Cfg<N, radix_for<N, 2>(), 2>>(inverse, ax, in, out, nlines, inner, s);
-  return launch_cfg<jtk::Cfg<N, radix_for<N, 4>(), 4>>(inverse, ax, in, out, nlines, inner, s);
+                   const jtk::Layout &lay, cudaStream_t s) {
+  if (maxr <= 2) return launch_cfg<jtk::Cfg<N, radix_for<N, 2>(), 2>>(inverse, ax, in, out, nlines, lay, s);
+  return launch_cfg<jtk::Cfg<N, radix_for<N, 4>(), 4>>(inverse, ax, in, out, nlines, lay, s);
 }
 
+// One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
+// layout of the slab all-to-all for the input / output.
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
-                      long long inner, cudaStream_t s) {
+                      long long inner, cudaStream_t s, int in_split = 1, int out_split = 1) {
   jtk::AxisDev ax = axis_dev(p, axis);
   const int maxr = p->dev[axis].maxr;
   const long long nlines = outer * inner;
+  const jtk::Layout lay{outer, inner, (int)(p->n[axis] / in_split), (int)(p->n[axis] / out_split)};
   switch (ax.N) {
-    case 16: return launch_n<16>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 32: return launch_n<32>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 64: return launch_n<64>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 128: return launch_n<128>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 256: return launch_n<256>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 512: return launch_n<512>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 1024: return launch_n<1024>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 2048: return launch_n<2048>(inverse, maxr, ax, in, out, nlines, inner, s);
-    case 4096: return launch_n<4096>(inverse, maxr, ax, in, out, nlines, inner, s);
+    case 16: return launch_n<16>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 32: return launch_n<32>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 64: return launch_n<64>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 128: return launch_n<128>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 256: return launch_n<256>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 512: return launch_n<512>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 1024: return launch_n<1024>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 2048: return launch_n<2048>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 4096: return launch_n<4096>(inverse, maxr, ax, in, out, nlines, lay, s);
     default: return fail(JT_ERR_ARG, "unsupported FFT length");
   }
 }
@@ -392,24 +395,34 @@ jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs
 }
 
 static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *in, double *out, int64_t outer,
-                            int64_t inner, void *stream) {
+                            int64_t inner, int in_split, int out_split, void *stream) {
   jt_status st = check_device_plan(p);
   if (st != JT_OK) return st;
   if (axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad axis");
   if (!in || !out || outer < 0 || inner < 1) return fail(JT_ERR_ARG, "bad pointers / shape");
-  if (overlaps_partially(in, out, outer * inner * p->n[axis])) return fail(JT_ERR_ARG, "partial overlap");
+  if (in_split < 1 || out_split < 1 || p->n[axis] % in_split != 0 || p->n[axis] % out_split != 0)
+    return fail(JT_ERR_ARG, "in_split / out_split must be >= 1 and divide n[axis]");
+  const int64_t count = outer * inner * p->n[axis];
+  if (overlaps_partially(in, out, count)) return fail(JT_ERR_ARG, "partial overlap");
+  if (in == out && (in_split != 1 || out_split != 1))
+    return fail(JT_ERR_ARG, "chunk-major layouts need out-of-place buffers");
   DeviceGuard g(p->device);
-  return launch_axis(p, axis, inverse, in, out, outer, inner, (cudaStream_t)stream);
+  return launch_axis(p, axis, inverse, in, out, outer, inner, (cudaStream_t)stream, in_split, out_split);
 }
 
 jt_status jt_forward_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer, int64_t inner,
                           void *stream) {
-  return axis_entry(p, axis, false, in, out, outer, inner, stream);
+  return axis_entry(p, axis, false, in, out, outer, inner, 1, 1, stream);
 }
 
 jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer, int64_t inner,
                           void *stream) {
-  return axis_entry(p, axis, true, in, out, outer, inner, stream);
+  return axis_entry(p, axis, true, in, out, outer, inner, 1, 1, stream);
+}
+
+jt_status jt_axis_pass(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
+                       int64_t inner, int in_split, int out_split, void *stream) {
+  return axis_entry(p, axis, inverse != 0, in, out, outer, inner, in_split, out_split, stream);
 }
 
 jt_status jt_destroy(jt_plan_t p) {

@@ -1,0 +1,170 @@
+"""Slab-distributed d-dimensional (d = 2, 3) transform over a torch.distributed process group
+(DESIGN.md §7).
+
+Every line of an axis pass is independent (the paper's "n 2D transforms and n^2 1D transforms",
+PAPER.md:724; "n 1D transforms" per axis in 2D), so the only exchange of the
+axis-factored schedule (eq:TJ PAPER.md:669-674, eq:TJ3 PAPER.md:718-722) is the transpose between
+passes.  Rank g of G holds
+
+    forward input  / inverse output: the x-slab  [g n0/G, (g+1) n0/G) x n1 (x n2)      (C-order)
+    forward output / inverse input:  the y-slab  n0 x [g n1/G, (g+1) n1/G) (x n2)      (C-order)
+
+Forward: the local axis passes d-1 .. 1, the axis-1 pass writing its output in the CHUNK-MAJOR layout
+(`out_split = G`, include/jt.h jt_axis_pass) so that chunk p is the contiguous block for rank p; one
+all-to-all (NCCL over NVLink on GPUs); the received buffer is already the C-order y-slab, on which the
+axis-0 pass runs.  Inverse: axis d-1 pass, axis-0 pass with `out_split = G`, all-to-all, axis-1 pass
+reading the chunk-major layout (`in_split = G`).  There is no pack / unpack kernel and no other
+collective.
+
+This module is host-side schedule only: every arithmetic step runs in libjt.so's kernels through
+`jt_axis_pass`; the exchange is `torch.distributed.all_to_all_single`.  For CPU tests of the schedule
+(gloo, world size > 1) an `axis_pass` callable with the same semantics may be injected.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class SlabPlan:
+    """Plan + buffers of one rank of a slab-distributed transform.
+
+    shape, a, b, eps: as for `Plan` (d = 2 or 3; shape[0] and shape[1] divisible by the world size).
+    dist:      the `torch.distributed` module (initialised); `group` an optional process group.
+    axis_pass: optional stand-in `f(axis, inverse, src, dst, outer, inner, in_split, out_split)`; default is
+               libjt.so's jt_axis_pass on the current CUDA stream.
+    """
+
+    def __init__(self, shape, a, b, eps, dist, group=None, axis_pass=None, device=None, **plan_kw):
+        import torch
+        self.shape = tuple(int(v) for v in shape)
+        self.d = len(self.shape)
+        if self.d not in (2, 3):
+            raise ValueError("slab decomposition needs d = 2 or 3")
+        self.dist = dist
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        n0, n1 = self.shape[0], self.shape[1]
+        if n0 % self.G or n1 % self.G:
+            raise ValueError(f"n0 = {n0} and n1 = {n1} must be divisible by the world size {self.G}")
+        self.rest = int(np.prod(self.shape[2:])) if self.d == 3 else 1
+        self.x_shape = (n0 // self.G, n1) + self.shape[2:]
+        self.y_shape = (n0, n1 // self.G) + self.shape[2:]
+        self.count = int(np.prod(self.x_shape))
+        self.plan = None
+        if axis_pass is None:
+            from . import Plan, jt_axis_pass
+            self.plan = Plan(self.shape, a, b, eps, **plan_kw)
+            self.ranks = [self.plan.rank(i) for i in range(self.d)]
+            handle = self.plan.handle
+
+            def axis_pass(axis, inverse, src, dst, outer, inner, in_split, out_split):
+                jt_axis_pass(handle, axis, inverse, src, dst, outer, inner, in_split, out_split)
+            self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        else:
+            self.ranks = None
+            self.device = torch.device("cpu") if device is None else device
+        self._axis = axis_pass
+        self._send = torch.empty(self.count, dtype=torch.float64, device=self.device)
+        self._recv = torch.empty(self.count, dtype=torch.float64, device=self.device)
+        self.launches_per_step = self.d  # axis passes (the all-to-all is NCCL's)
+
+    # ---- geometry ----
+    def local_box(self, which: int):
+        """(lo, hi) index box of this rank's block: which = 0 forward input (x-slab), 1 forward output."""
+        lo = [0] * self.d
+        hi = list(self.shape)
+        ax = 0 if which == 0 else 1
+        step = self.shape[ax] // self.G
+        lo[ax], hi[ax] = self.rank * step, (self.rank + 1) * step
+        return tuple(lo), tuple(hi)
+
+    def local_input(self, full):
+        """This rank's x-slab of a full (host) array, as a contiguous tensor on the plan's device."""
+        import torch
+        lo, hi = self.local_box(0)
+        t = torch.as_tensor(full)[lo[0]:hi[0]].contiguous()
+        return t.to(self.device)
+
+    def local_output(self, full):
+        """This rank's y-slab of a full array (e.g. for the inverse's input)."""
+        import torch
+        lo, hi = self.local_box(1)
+        t = torch.as_tensor(full)[:, lo[1]:hi[1]].contiguous()
+        return t.to(self.device)
+
+    # ---- exchange ----
+    def _exchange(self):
+        if self.G == 1:
+            self._recv.copy_(self._send)
+        else:
+            self.dist.all_to_all_single(self._recv, self._send, group=self.group)
+
+    # ---- transforms ----
+    def forward(self, x, out=None):
+        """x-slab coefficients -> y-slab weighted values (the local block of Phi_0 (x) ... (x) Phi_{d-1} alpha)."""
+        out = self.forward_local(x, out)
+        self._exchange()
+        return self.forward_finish(out)
+
+    def forward_local(self, x, out=None):
+        """Forward phase 1: the local axis passes d-1 .. 1; leaves the chunk-major send buffer filled."""
+        import torch
+        if tuple(x.shape) != self.x_shape:
+            raise ValueError(f"expected the x-slab shape {self.x_shape}")
+        out = torch.empty(self.y_shape, dtype=torch.float64, device=self.device) if out is None else out
+        G, (n0, n1), r = self.G, self.shape[:2], self.rest
+        if self.d == 3:
+            self._axis(2, False, x, out, (n0 // G) * n1, 1, 1, 1)                  # axis 2, tmp in `out`
+            self._axis(1, False, out, self._send, n0 // G, r, 1, G)              # axis 1 -> chunk-major
+        else:
+            self._axis(1, False, x, self._send, n0 // G, 1, 1, G)
+        return out
+
+    def forward_finish(self, out):
+        """Forward phase 2 (after the all-to-all): the axis-0 pass on the received y-slab."""
+        G, (n0, n1), r = self.G, self.shape[:2], self.rest
+        self._axis(0, False, self._recv, out, 1, (n1 // G) * r, 1, 1)
+        return out
+
+    def inverse(self, y, out=None):
+        """y-slab weighted values -> x-slab coefficients (transpose in every axis)."""
+        out = self.inverse_local(y, out)
+        self._exchange()
+        return self.inverse_finish(out)
+
+    def inverse_local(self, y, out=None):
+        """Inverse phase 1: axis d-1 pass, axis-0 pass into the chunk-major send buffer."""
+        import torch
+        if tuple(y.shape) != self.y_shape:
+            raise ValueError(f"expected the y-slab shape {self.y_shape}")
+        out = torch.empty(self.x_shape, dtype=torch.float64, device=self.device) if out is None else out
+        G, (n0, n1), r = self.G, self.shape[:2], self.rest
+        if self.d == 3:
+            self._axis(2, True, y, out, n0 * (n1 // G), 1, 1, 1)                  # axis 2, tmp in `out`
+            self._axis(0, True, out, self._send, 1, (n1 // G) * r, 1, G)         # axis 0 -> chunk-major
+        else:
+            self._axis(0, True, y, self._send, 1, n1 // G, 1, G)
+        return out
+
+    def inverse_finish(self, out):
+        """Inverse phase 2 (after the all-to-all): the axis-1 pass reading the chunk-major receive buffer."""
+        G, (n0, n1), r = self.G, self.shape[:2], self.rest
+        self._axis(1, True, self._recv, out, n0 // G, r, G, 1)
+        return out
+
+    def make_forward_step(self, x):
+        """Closure running one forward transform of the resident x-slab into a preallocated y-slab."""
+        import torch
+        out = torch.empty(self.y_shape, dtype=torch.float64, device=self.device)
+
+        def step():
+            self.forward(x, out)
+            return out
+        step.out = out
+        return step
+
+    def close(self):
+        if self.plan is not None:
+            self.plan.close()
+            self.plan = None

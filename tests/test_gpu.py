@@ -192,3 +192,65 @@ def test_partial_overlap_rejected():
     with pytest.raises(jt.JTError) as ei:
         jt.jt_forward(p.handle, buf[:64], buf[8:72])
     assert ei.value.status == jt.JT_ERR_ARG
+
+
+class _VirtualDist:
+    """get_world_size / get_rank of one virtual rank (no collective is ever called: the test does the
+    exchange itself between phases, so no kernel waits on another)."""
+
+    def __init__(self, rank, world):
+        self.r, self.w = rank, world
+
+    def get_world_size(self, group=None):
+        return self.w
+
+    def get_rank(self, group=None):
+        return self.r
+
+
+@pytest.mark.parametrize("world,shape,a,b", [
+    (4, (64, 48, 40), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)),
+    (8, (96, 64, 33), (0.25, -0.1, 0.0), (-0.25, 0.6, 0.0)),
+    (2, (256, 256), (0.1, -0.25), (-0.4, 0.35)),
+    (8, (512, 64, 16), (0.25, 0.25, 0.25), (-0.25, -0.25, -0.25)),
+])
+def test_chunk_major_layouts_virtual_ranks(world, shape, a, b):
+    """The slab schedule (paper_1901_07275_b200/dist.py) on one GPU with `world` virtual ranks run one
+    after another: the kernels' chunk-major output (out_split) and input (in_split) layouts plus a
+    tensor-copy all-to-all must reproduce the oracle's full transform, block by block."""
+    from paper_1901_07275_b200.dist import SlabPlan
+    sps = [SlabPlan(shape, a, b, 1e-12, _VirtualDist(g, world)) for g in range(world)]
+    x = si.gaussian(shape, seed=11)
+    ref = oracle.forward(x, a, b)
+    c = sps[0].count // world
+
+    def exchange():
+        for g in range(world):
+            sps[g]._recv.copy_(torch.cat([sps[q]._send[g * c:(g + 1) * c] for q in range(world)]))
+
+    outs = [sp.forward_local(sp.local_input(x)) for sp in sps]
+    exchange()
+    ys = [sp.forward_finish(o) for sp, o in zip(sps, outs)]
+    y_full = np.concatenate([y.cpu().numpy() for y in ys], axis=1)
+    assert relerr(y_full, ref) <= TOL
+    # inverse from the y-slabs back to x-slabs
+    outs = [sp.inverse_local(y) for sp, y in zip(sps, ys)]
+    exchange()
+    zs = [sp.inverse_finish(o) for sp, o in zip(sps, outs)]
+    z_full = np.concatenate([z.cpu().numpy() for z in zs], axis=0)
+    assert relerr(z_full, x) <= TOL
+    for sp in sps:
+        sp.close()
+
+
+def test_axis_pass_split_arguments_rejected():
+    p = jt.Plan((12, 10), (0.1, 0.2), (0.0, 0.1), 1e-12)
+    x = torch.zeros(120, dtype=torch.float64, device="cuda")
+    y = torch.zeros_like(x)
+    for args in [(0, 5, 1), (0, 1, 5), (1, 0, 1)]:  # 5 does not divide 12; split 0
+        ax, isp, osp = args
+        with pytest.raises(jt.JTError) as ei:
+            jt.jt_axis_pass(p.handle, ax, False, x, y, 1, 10 if ax == 0 else 1, isp, osp)
+        assert ei.value.status == jt.JT_ERR_ARG
+    with pytest.raises(jt.JTError):  # chunk-major in place
+        jt.jt_axis_pass(p.handle, 0, False, x, x, 1, 10, 1, 2)
