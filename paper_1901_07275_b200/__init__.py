@@ -18,7 +18,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjt.so")
+# JT_LIB: path of an alternative in-tree build (kernel A/B experiments, tools/); default libjt.so
+LIB_PATH = os.environ.get("JT_LIB") or os.path.join(_HERE, "libjt.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1901_07275_b200.build` "
                       "(there is deliberately no fallback path)")

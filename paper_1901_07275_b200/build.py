@@ -28,21 +28,22 @@ def _run(cmd):
     subprocess.run(cmd, check=True)
 
 
-def build(verbose_ptxas: bool = False) -> str:
+def build(verbose_ptxas: bool = False, out: str = LIB, defines=(), tag: str = "") -> str:
+    """Compile libjt.so (or a variant: `out` path, extra -D `defines`, object-file `tag`)."""
     nvcc = _nvcc()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     build_dir = os.path.join(HERE, "_build")
     os.makedirs(build_dir, exist_ok=True)
     plan_o = os.path.join(build_dir, "plan.o")
-    api_o = os.path.join(build_dir, "jt_api.o")
+    api_o = os.path.join(build_dir, f"jt_api{tag}.o")
     _run(["g++", "-std=c++17", "-O2", "-fPIC", "-fopenmp", *inc, "-c", os.path.join(CSRC, "plan.cpp"),
           "-o", plan_o])
-    flags = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", *inc]
+    flags = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", *inc, *[f"-D{d}" for d in defines]]
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]
     _run([nvcc, *flags, "-c", os.path.join(CSRC, "jt_api.cu"), "-o", api_o])
-    _run([nvcc, *ARCH, "-shared", "-o", LIB, api_o, plan_o, "-Xcompiler", "-fopenmp", "-lgomp"])
-    return LIB
+    _run([nvcc, *ARCH, "-shared", "-o", out, api_o, plan_o, "-Xcompiler", "-fopenmp", "-lgomp"])
+    return out
 
 
 if __name__ == "__main__":

@@ -110,22 +110,29 @@ struct Cfg {
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;
   static constexpr int PSLOTS = PRIV ? (R > NB * MAXR ? R : NB * MAXR) : 0;  // private doubles per thread
-  static constexpr int GROUP_BYTES = ((SLOTS * XB + K0MAX * LG * 8 + PSLOTS * GT * 8) + 127) / 128 * 128;
-  // factor ring: stage = v_l (N complex) + u~_l (MAXR x NBINS complex)
+  // + the inverse's per-warp partial sums of (W V)^T y (K0MAX x GW x LG)
+  static constexpr int GROUP_BYTES = ((SLOTS * XB + K0MAX * LG * 8 + PSLOTS * GT * 8 + K0MAX * GW * LG * 8) + 127) / 128 * 128;
+  // factor ring: stage = v_l (N complex) + u~_l (MAXR x NBINS complex) [+ KPT columns of W V (forward, VST):
+  // the dense low-degree block is applied inside the term loop, KPT degrees per term, from SMEM]
   static constexpr bool STAGED = N <= 1024;
+  static constexpr bool VST = N <= 512;
+  static constexpr int KPT = VST ? 2 : 0;
   static constexpr int NSTAGE = 2;
-  static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16;
-  static constexpr int STAGE_BYTES = STAGED ? (V_BYTES + U_BYTES + 127) / 128 * 128 : 0;
+  static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
+  static constexpr int STAGE_BYTES = STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : 0;
   static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
+  // per-CTA table of the row range of every (thread position vt, bin slot q): (j0 << 4) | count
+  static constexpr int BINFO_BYTES = STAGED ? (TPL * NB * 4 + 127) / 128 * 128 : 0;
+  static constexpr int HDR_BYTES = (RING_BYTES + 127) / 128 * 128 + BINFO_BYTES;
   static constexpr int gpc_fit(int g) {
-    return (g > 1 && (((g * GT + 127) / 128) * 128 * REGS > 65536 || g * GROUP_BYTES + RING_BYTES + 256 > SMEM_LIMIT || g * GW > 15 ||
+    return (g > 1 && (((g * GT + 127) / 128) * 128 * REGS > 65536 || g * GROUP_BYTES + HDR_BYTES > SMEM_LIMIT || g * GW > 15 ||
                       g * GT > 1024))
                ? gpc_fit(g - 1)
                : g;
   }
   static constexpr int GPC = gpc_fit(8);  // groups per CTA (one CTA per SM)
   static constexpr int NT = GPC * GT;      // threads per CTA
-  static constexpr size_t smem_bytes() { return (size_t)RING_BYTES + 256 + (size_t)GPC * GROUP_BYTES; }
+  static constexpr size_t smem_bytes() { return (size_t)HDR_BYTES + (size_t)GPC * GROUP_BYTES; }
   __device__ static __forceinline__ int sidx(int pos, int line) { return (pos + pos / R) * LG + line; }
   static_assert(GT % 32 == 0, "group must be whole warps");
   static_assert(RSL >= 2, "last pass radix");
@@ -178,19 +185,28 @@ struct Ring {
   uint64_t *full, *empty;
   long long total;  // terms this CTA will consume
   const double2 *gv, *gu;
-  int r;
+  const double *gph;
+  int r, k0;
   __device__ __forceinline__ double2 *v(long long seq) const {
     return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES);
   }
   __device__ __forceinline__ double2 *u(long long seq) const {
     return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::V_BYTES);
   }
+  __device__ __forceinline__ const double *ph(long long seq) const {
+    return reinterpret_cast<const double *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::V_BYTES + C::U_BYTES);
+  }
   __device__ __forceinline__ void issue(long long seq) const {  // producer: one thread
     const int s = (int)(seq % C::NSTAGE);
     const int l = (int)(seq % r);
-    mbar_arrive_expect_tx(&full[s], C::V_BYTES + C::U_BYTES);
+    int kc = 0;
+    if constexpr (C::VST) kc = min(C::KPT, max(0, k0 - l * C::KPT));
+    const uint32_t ph_bytes = (uint32_t)kc * C::MAXR * C::NBINS * 8;
+    mbar_arrive_expect_tx(&full[s], C::V_BYTES + C::U_BYTES + ph_bytes);
     tma_load_1d(v(seq), gv + (long long)l * C::N, C::V_BYTES, &full[s]);
     tma_load_1d(u(seq), gu + (long long)l * C::MAXR * C::NBINS, C::U_BYTES, &full[s]);
+    if (kc > 0)
+      tma_load_1d(const_cast<double *>(ph(seq)), gph + (long long)l * C::KPT * C::MAXR * C::NBINS, ph_bytes, &full[s]);
   }
   __device__ __forceinline__ void wait_full(long long seq) const {
     mbar_wait(&full[seq % C::NSTAGE], (uint32_t)((seq / C::NSTAGE) & 1));
@@ -357,6 +373,7 @@ struct Ctx {
   void *buf;     // group exchange buffer
   double *alow;  // group: k0 x LG low-degree coefficients (forward) / reduced a_V (inverse)
   double *priv;  // group: thread-private slots [slot][gt] (C::PRIV)
+  double *vred;  // group: K0MAX x GW x LG per-warp partials of (W V)^T y (inverse)
   Ring<C> ring;
   long long nbatch;
   const double2 *gv, *gu;
@@ -373,16 +390,37 @@ struct Ctx {
     ring.gv = ax.v;
     ring.gu = ax.ub;
     ring.r = ax.r;
-    char *gb = smem + ((C::RING_BYTES + 127) / 128) * 128 + grp * C::GROUP_BYTES;
+    ring.gph = ax.phivb;
+    ring.k0 = ax.k0;
+    char *gb = smem + C::HDR_BYTES + grp * C::GROUP_BYTES;
     buf = gb;
     alow = reinterpret_cast<double *>(gb + C::SLOTS * C::XB);
     priv = alow + K0MAX * C::LG;
+    vred = priv + C::PSLOTS * C::GT;
     nbatch = (nlines + C::GPC * C::LG - 1) / (C::GPC * C::LG);
     const long long mine = blockIdx.x < nbatch ? (nbatch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     ring.total = mine * ax.r;
   }
-  // Ring set-up: barriers initialised and the first NSTAGE terms in flight before anyone waits.
-  __device__ __forceinline__ void start() {
+  // CTA table: TPL x NB packed row ranges (j0 << 4) | count of the bins binof(vt, q) (staged configs;
+  // the others read bstart from global: their register budget has no room for the extra live state)
+  __device__ static __forceinline__ int *binfo() {
+    extern __shared__ __align__(128) char smem_raw[];
+    return reinterpret_cast<int *>(smem_raw + ((C::RING_BYTES + 127) / 128) * 128);
+  }
+  __device__ __forceinline__ void rows_of(const int *__restrict__ bstart, int q, int m, int &j0, int &cnt) const {
+    if constexpr (C::STAGED) {
+      const int bi = binfo()[vt * C::NB + q];
+      j0 = bi >> 4;
+      cnt = bi & 15;
+    } else {
+      j0 = __ldg(&bstart[m]);
+      cnt = __ldg(&bstart[m + 1]) - j0;
+    }
+  }
+  // Ring set-up: barriers initialised and the first NSTAGE terms in flight before anyone waits; the
+  // row-range table of the bins binof(vt, q) filled.
+  template <class BinOf>
+  __device__ __forceinline__ void start(const int *__restrict__ bstart, BinOf binof) {
     if constexpr (C::STAGED) {
       if (threadIdx.x == 0) {
         for (int s = 0; s < C::NSTAGE; ++s) {
@@ -392,8 +430,13 @@ struct Ctx {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (long long q = 0; q < C::NSTAGE && q < ring.total; ++q) ring.issue(q);
       }
-      __syncthreads();
     }
+    if constexpr (C::STAGED) for (int i = threadIdx.x; i < C::TPL * C::NB; i += C::NT) {
+      const int m = binof(i / C::NB, i % C::NB);
+      const int j0 = __ldg(&bstart[m]);
+      binfo()[i] = (j0 << 4) | (__ldg(&bstart[m + 1]) - j0);
+    }
+    __syncthreads();
   }
   __device__ __forceinline__ const double2 *vfac(long long seq, int l) const {
     if constexpr (C::STAGED) return ring.v(seq);
@@ -445,35 +488,38 @@ struct Layout {
   int in_cs, out_cs;  // chunk length of the input / output along the axis (== n: plain C-order)
 };
 
+// SPLIT is a template flag (a separate kernel instantiation) so that the plain layout costs no registers.
+template <bool SPLIT>
 struct LineAddr {
   long long b0, cstride, inner;
   int cs;
-  bool plain;
   __device__ __forceinline__ LineAddr(long long L, long long outer, long long inner_, int n, int cs_) {
     const long long o = L / inner_, i = L - o * inner_;
     inner = inner_;
-    cs = cs_;
-    plain = cs_ == n;
-    b0 = o * (long long)cs_ * inner_ + i;
-    cstride = outer * (long long)cs_ * inner_;
+    cs = SPLIT ? cs_ : n;
+    b0 = o * (long long)cs * inner_ + i;
+    cstride = SPLIT ? outer * (long long)cs * inner_ : 0;
   }
   __device__ __forceinline__ long long at(int j) const {
-    return plain ? b0 + (long long)j * inner : b0 + (long long)(j / cs) * cstride + (long long)(j % cs) * inner;
+    if constexpr (SPLIT) return b0 + (long long)(j / cs) * cstride + (long long)(j % cs) * inner;
+    else return b0 + (long long)j * inner;
   }
 };
 
 // ------------------------------------------------------------------------------------------------
 // Forward axis pass (K4).
 // ------------------------------------------------------------------------------------------------
-template <class C>
+template <class C, bool SPLIT>
 __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
                                                              long long nlines, Layout lay) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C> cx(smem_raw, ax, nlines);
-  cx.start();
+  cx.start(ax.bstart, [](int vt_, int q) { return q < R / 2 ? out_pos<C>(vt_, fwd_reg_of_bin<C>(q)) : C::N / 2; });
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
+  // degrees [0, kin) of W V are applied inside the term loop from the ring (KPT per term), the rest here
+  const int kin = C::VST ? min(k0, ax.r * C::KPT) : 0;
 
   int m[NB];
 #pragma unroll
@@ -483,17 +529,25 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
-    const LineAddr oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
 
     // coefficients at the first-pass input positions k = vt + r TPL; degrees < k0 also to alow
+    // (all loads issued before any shared-memory store, so that their latencies overlap)
     State<C, R> a(cx.priv, cx.gt);
+    {
+      double av[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int k = vt + r * TPL;
-      const double ak = (live && k < n) ? in[ia.at(k)] : 0.0;
-      a.set(r, ak);
-      if (r * TPL < K0MAX && k < k0) cx.alow[k * LG + line] = ak;
+      for (int r = 0; r < R; ++r) {
+        const int k = vt + r * TPL;
+        av[r] = (live && k < n) ? __ldg(&in[ia.at(k)]) : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int k = vt + r * TPL;
+        a.set(r, av[r]);
+        if (r * TPL < K0MAX && k < k0) cx.alow[k * LG + line] = av[r];
+      }
     }
 
     // A4: y = W V a_V on the rows of the thread's bins
@@ -503,7 +557,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int c = 0; c < MAXR; ++c) y[q][c] = 0.0;
     group_sync<C>();
-    for (int k = 0; k < k0; ++k) {
+    for (int k = kin; k < k0; ++k) {
       const double ak = cx.alow[k * LG + line];
       const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
 #pragma unroll
@@ -519,6 +573,20 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       cx.acquire(seq);
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
+      if constexpr (C::VST) {  // A4 for degrees l KPT .. l KPT + KPT - 1 (rows of W V staged with the term)
+        const double *ph = cx.ring.ph(seq);
+#pragma unroll
+        for (int kk = 0; kk < C::KPT; ++kk) {
+          const int k = l * C::KPT + kk;
+          if (k < k0) {
+            const double ak = cx.alow[k * LG + line];
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+#pragma unroll
+              for (int c = 0; c < MAXR; ++c) y[q][c] = fma(ph[(kk * MAXR + c) * NBINS + m[q]], ak, y[q][c]);
+          }
+        }
+      }
       double xr[R], xi[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {  // A1
@@ -546,7 +614,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         if (q < R / 2 || vt == 0) {
-          const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
+          int j0, cnt;
+          cx.rows_of(ax.bstart, q, m[q], j0, cnt);
 #pragma unroll
           for (int c = 0; c < MAXR; ++c)
             if (c < cnt) out[oa.at(j0 + c)] = y[q][c];
@@ -560,15 +629,18 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 // ------------------------------------------------------------------------------------------------
 // Inverse axis pass (K5).
 // ------------------------------------------------------------------------------------------------
-template <class C>
+template <class C, bool SPLIT>
 __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const double *in, double *out,
                                                              long long nlines, Layout lay) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C> cx(smem_raw, ax, nlines);
-  cx.start();
+  cx.start(ax.bstart, [](int vt_, int q) { return q < R / 2 ? vt_ + q * TPL : C::N / 2; });
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
+  // degrees [0, kin) of (W V)^T y are formed inside the term loop from the ring (KPT per term), the rest
+  // at batch start
+  const int kin = C::VST ? min(k0, ax.r * C::KPT) : 0;
 
   // input bins: q < R/2 -> first-pass position vt + q TPL; q = R/2 -> position vt + N/2 (Nyquist, vt == 0)
   int m[NB];
@@ -579,8 +651,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
-    const LineAddr oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
 
     State<C, NB * MAXR> yb(cx.priv, cx.gt);  // yb(q MAXR + c): row c of input bin q
     {
@@ -591,15 +663,15 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         const bool own = q < R / 2 || vt == 0;
-        const int j0 = __ldg(&ax.bstart[m[q]]), cnt = __ldg(&ax.bstart[m[q] + 1]) - j0;
+        int j0, cnt;
+        cx.rows_of(ax.bstart, q, m[q], j0, cnt);
 #pragma unroll
-        for (int c = 0; c < MAXR; ++c) {
-          yr[q * MAXR + c] = (live && own && c < cnt) ? in[ia.at(j0 + c)] : 0.0;
-          yb.set(q * MAXR + c, yr[q * MAXR + c]);
-        }
+        for (int c = 0; c < MAXR; ++c) yr[q * MAXR + c] = (live && own && c < cnt) ? __ldg(&in[ia.at(j0 + c)]) : 0.0;
       }
+#pragma unroll
+      for (int i = 0; i < NB * MAXR; ++i) yb.set(i, yr[i]);
       double *red = static_cast<double *>(cx.buf);  // k0 x GW x LG partials (exchange buffer is free)
-      for (int k = 0; k < k0; ++k) {
+      for (int k = kin; k < k0; ++k) {
         const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
         double p = 0.0;
 #pragma unroll
@@ -619,7 +691,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       if constexpr (C::GW > 1) {
         group_sync<C>();
-        for (int i = cx.gt; i < k0 * LG; i += C::GT) {
+        for (int i = cx.gt + kin * LG; i < k0 * LG; i += C::GT) {
           const int k = i / LG, ln = i % LG;
           double s = 0.0;
 #pragma unroll
@@ -639,6 +711,11 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
       double xr[R], xi[R];
+      double pv[C::VST ? C::KPT : 1];  // partial (W V)^T y for degrees l KPT + kk (VST)
+#pragma unroll
+      for (int kk = 0; kk < (C::VST ? C::KPT : 1); ++kk) pv[kk] = 0.0;
+      const double *ph = C::VST ? cx.ring.ph(seq) : nullptr;
+      const int kb = l * C::KPT;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         xr[r] = 0.0;
@@ -650,6 +727,26 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
             const double yv = yb.get(r * MAXR + c);
             xr[r] = fma(uu.x, yv, xr[r]);
             xi[r] = fma(uu.y, yv, xi[r]);
+            if constexpr (C::VST) {
+#pragma unroll
+              for (int kk = 0; kk < C::KPT; ++kk)
+                if (kb + kk < k0) pv[kk] = fma(ph[(kk * MAXR + c) * NBINS + m[r]], yv, pv[kk]);
+            }
+          }
+        }
+      }
+      if constexpr (C::VST) {  // reduce over the line's threads: shuffles in the warp, per-warp slots after
+#pragma unroll
+        for (int kk = 0; kk < C::KPT; ++kk) {
+          if (kb + kk < k0) {
+            double p = pv[kk];
+#pragma unroll
+            for (int off = LG; off < 32; off *= 2) p += __shfl_xor_sync(0xffffffffu, p, off);
+            if constexpr (C::GW == 1) {
+              if (vt == 0) cx.alow[(kb + kk) * LG + line] = p;
+            } else {
+              if ((threadIdx.x & 31) < LG) cx.vred[((kb + kk) * C::GW + (cx.gt >> 5)) * LG + line] = p;
+            }
           }
         }
       }
@@ -662,6 +759,16 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       group_sync<C>();
       cx.release(seq);
+    }
+    if constexpr (C::VST && C::GW > 1) {  // combine the per-warp partials of degrees < kin
+      for (int i = cx.gt; i < kin * LG; i += C::GT) {
+        const int k = i / LG, ln = i % LG;
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < C::GW; ++w) s += cx.vred[(k * C::GW + w) * LG + ln];
+        cx.alow[k * LG + ln] = s;
+      }
+      group_sync<C>();
     }
 
     if (live) {

@@ -104,12 +104,13 @@ jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, dou
   JT_CUDA_TRY(cudaGetDevice(&dev));
   JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const unsigned grid = (unsigned)std::min<long long>(batches, sms);
+  const bool split = lay.in_cs != ax.n || lay.out_cs != ax.n;
   if (inverse) {
-    auto kern = jtk::inv_axis_kernel<C>;
+    auto kern = split ? jtk::inv_axis_kernel<C, true> : jtk::inv_axis_kernel<C, false>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay);
   } else {
-    auto kern = jtk::fwd_axis_kernel<C>;
+    auto kern = split ? jtk::fwd_axis_kernel<C, true> : jtk::fwd_axis_kernel<C, false>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay);
   }
