@@ -50,6 +50,8 @@ struct AxisDev {
   const double2 *v;      // r x N        v_l[k] at v[l N + k] (zero for k < k0 and k >= n)
   const double2 *ub;     // r x MAXR x nbins   u~_l of row bstart[m] + c at ub[(l MAXR + c) nbins + m] (0-padded)
   const double *phivb;   // k0 x MAXR x nbins  (W V)[bstart[m] + c, k] at phivb[(k MAXR + c) nbins + m] (0-padded)
+  const double *phivc;   // the same in chunks of 2 degrees: (W V)[bstart[m] + c, 2 l + kk] at
+                         // phivc[((l nbins + m) MAXR + c) 2 + kk], l < ceil(k0 / 2) (0-padded)
   const int *bstart;     // nbins + 1 row offsets: rows of bin m are bstart[m] .. bstart[m+1]-1
   const double2 *tw;     // per-pass twiddle tables, see TwOff (pass NS, radix RS: (RS-1) NS entries,
                          // entry (r-1) NS + j = e^{+2 pi i j r / (NS RS)})
@@ -86,9 +88,20 @@ struct TwOff<N, R, NS, N> {
   static constexpr int value = 0;
 };
 
-template <int N_, int R_, int MAXR_>
+// Total entries of the per-pass twiddle tables (TwOff of the pass after the last).
+template <int N, int R, int P = Pass<N, R, 1>::RS>
+struct TwTotal {
+  static constexpr int value = (Pass<N, R, P>::RS - 1) * P + TwTotal<N, R, P * Pass<N, R, P>::RS>::value;
+};
+template <int N, int R>
+struct TwTotal<N, R, N> {
+  static constexpr int value = 0;
+};
+
+template <int N_, int R_, int MAXR_, bool INV_>
 struct Cfg {
   static constexpr int N = N_, R = R_, MAXR = MAXR_;
+  static constexpr bool INV = INV_;
   static constexpr int TPL = N / R;                                     // threads per line
   static constexpr int LG = TPL <= 8 ? 32 / TPL : (TPL <= 32 ? 4 : 1);  // lines per group
   static constexpr int GT = TPL * LG;                                   // threads per group
@@ -110,33 +123,50 @@ struct Cfg {
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;
   static constexpr int PSLOTS = PRIV ? (R > NB * MAXR ? R : NB * MAXR) : 0;  // private doubles per thread
-  // + the inverse's per-warp partial sums of (W V)^T y (K0MAX x GW x LG)
-  static constexpr int GROUP_BYTES = ((SLOTS * XB + K0MAX * LG * 8 + PSLOTS * GT * 8 + K0MAX * GW * LG * 8) + 127) / 128 * 128;
-  // factor ring: stage = v_l (N complex) + u~_l (MAXR x NBINS complex) [+ KPT columns of W V (forward, VST):
-  // the dense low-degree block is applied inside the term loop, KPT degrees per term, from SMEM]
+  // + (inverse) the per-warp partial sums of (W V)^T y (K0MAX x GW x LG)
+  static constexpr int VRED = INV ? K0MAX * GW * LG : 0;
+  static constexpr int GROUP_BYTES = ((SLOTS * XB + K0MAX * LG * 8 + PSLOTS * GT * 8 + VRED * 8) + 127) / 128 * 128;
+  // factor ring: stage = v_l (N complex) + u~_l (MAXR x NBINS complex) [+ chunk l of W V (VST): KPT degrees,
+  // layout [m][c][kk], so the dense low-degree block is applied inside the term loop from SMEM]
   static constexpr bool STAGED = N <= 1024;
   static constexpr bool VST = N <= 512;
   static constexpr int KPT = VST ? 2 : 0;
-  static constexpr int NSTAGE = 2;
   static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
   static constexpr int STAGE_BYTES = STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : 0;
-  static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
+  // twiddle tables of the passes after the first, copied to SMEM (TWS): every twiddle is one broadcast
+  // LDS.128 instead of a chain of complex multiplies
+  static constexpr bool TWS = N <= 1024;
+  static constexpr int TW_BYTES = TWS ? (TwTotal<N, R>::value * 16 + 127) / 128 * 128 : 0;
   // per-CTA table of the row range of every (thread position vt, bin slot q): (j0 << 4) | count
   static constexpr int BINFO_BYTES = STAGED ? (TPL * NB * 4 + 127) / 128 * 128 : 0;
-  static constexpr int HDR_BYTES = (RING_BYTES + 127) / 128 * 128 + BINFO_BYTES;
-  static constexpr int gpc_fit(int g) {
-    return (g > 1 && (((g * GT + 127) / 128) * 128 * REGS > 65536 || g * GROUP_BYTES + HDR_BYTES > SMEM_LIMIT || g * GW > 15 ||
-                      g * GT > 1024))
-               ? gpc_fit(g - 1)
+  static constexpr int hdr_bytes(int nstage) {
+    return (nstage * STAGE_BYTES + 3 * nstage * 8 + 127) / 128 * 128 + BINFO_BYTES + TW_BYTES;
+  }
+  static constexpr int gpc_fit(int g, int nstage) {
+    return (g > 1 && (((g * GT + 127) / 128) * 128 * REGS > 65536 || g * GROUP_BYTES + hdr_bytes(nstage) > SMEM_LIMIT ||
+                      g * GW > 15 || g * GT > 1024))
+               ? gpc_fit(g - 1, nstage)
                : g;
   }
-  static constexpr int GPC = gpc_fit(8);  // groups per CTA (one CTA per SM)
-  static constexpr int NT = GPC * GT;      // threads per CTA
+  static constexpr int GPC = gpc_fit(8, 2);  // groups per CTA (one CTA per SM)
+  // a third ring stage when it fits next to the GPC groups
+  static constexpr int NSTAGE = (STAGED && GPC * GROUP_BYTES + hdr_bytes(3) <= SMEM_LIMIT) ? 3 : 2;
+  static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES + 3 * NSTAGE * 8;  // stages + full/empty barriers + counters
+  static constexpr int BINFO_OFF = (RING_BYTES + 127) / 128 * 128;
+  static constexpr int TW_OFF = BINFO_OFF + BINFO_BYTES;
+  static constexpr int HDR_BYTES = hdr_bytes(NSTAGE);
+  static constexpr int NT = GPC * GT;  // threads per CTA
   static constexpr size_t smem_bytes() { return (size_t)HDR_BYTES + (size_t)GPC * GROUP_BYTES; }
   __device__ static __forceinline__ int sidx(int pos, int line) { return (pos + pos / R) * LG + line; }
   static_assert(GT % 32 == 0, "group must be whole warps");
   static_assert(RSL >= 2, "last pass radix");
+  static_assert(smem_bytes() <= SMEM_LIMIT, "shared memory");
 };
+
+__device__ __forceinline__ const double2 *tw_smem_base(int off) {
+  extern __shared__ __align__(128) char smem_raw[];
+  return reinterpret_cast<const double2 *>(smem_raw + off);
+}
 
 template <class C>
 __device__ __forceinline__ void group_sync() {
@@ -183,6 +213,7 @@ template <class C>
 struct Ring {
   char *base;
   uint64_t *full, *empty;
+  unsigned *cnt;    // per stage: groups that released it in the current phase (the last one refills it)
   long long total;  // terms this CTA will consume
   const double2 *gv, *gu;
   const double *gph;
@@ -199,28 +230,38 @@ struct Ring {
   __device__ __forceinline__ void issue(long long seq) const {  // producer: one thread
     const int s = (int)(seq % C::NSTAGE);
     const int l = (int)(seq % r);
-    int kc = 0;
-    if constexpr (C::VST) kc = min(C::KPT, max(0, k0 - l * C::KPT));
-    const uint32_t ph_bytes = (uint32_t)kc * C::MAXR * C::NBINS * 8;
+    const bool kc = C::VST && l * C::KPT < k0;  // chunk l of W V exists (zero-padded to KPT degrees)
+    const uint32_t ph_bytes = kc ? C::PH_BYTES : 0;
     mbar_arrive_expect_tx(&full[s], C::V_BYTES + C::U_BYTES + ph_bytes);
     tma_load_1d(v(seq), gv + (long long)l * C::N, C::V_BYTES, &full[s]);
     tma_load_1d(u(seq), gu + (long long)l * C::MAXR * C::NBINS, C::U_BYTES, &full[s]);
-    if (kc > 0)
+    if (kc)
       tma_load_1d(const_cast<double *>(ph(seq)), gph + (long long)l * C::KPT * C::MAXR * C::NBINS, ph_bytes, &full[s]);
   }
   __device__ __forceinline__ void wait_full(long long seq) const {
     mbar_wait(&full[seq % C::NSTAGE], (uint32_t)((seq / C::NSTAGE) & 1));
     __syncwarp();  // lanes may leave the try_wait loop in different iterations: reconverge
   }
-  // called by every thread of every group after its end-of-term group_sync
+  // Called by every thread of every group after its end-of-term group_sync.  The group's thread 0 counts the
+  // release; the LAST group to release the stage refills it (no thread ever blocks on the slowest group).
+  // The counter is a CTA-scope acq_rel atomic: every group's reads of the stage happen before its
+  // increment, the refill after the last one; the proxy fence orders those generic-proxy reads before
+  // the async-proxy (TMA) writes of the refill.
   __device__ __forceinline__ void release(long long seq, int gt) const {
-    if (gt == 0) mbar_arrive(&empty[seq % C::NSTAGE]);
-    if (threadIdx.x == 0 && seq + C::NSTAGE < total) {
-      mbar_wait(&empty[seq % C::NSTAGE], (uint32_t)((seq / C::NSTAGE) & 1));
-      issue(seq + C::NSTAGE);
+    if (gt == 0) {
+      const int s = (int)(seq % C::NSTAGE);
+      unsigned old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&cnt[s])) : "memory");
+      if (old == C::GPC - 1) {
+        cnt[s] = 0;
+        if (seq + C::NSTAGE < total) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(seq + C::NSTAGE);
+        }
+      }
     }
-    // reconverge warp 0 before the group's next (warp-aligned) bar.sync: bar.sync from a diverged warp
-    // is undefined and released the barrier early (a race seen on 512^3 axis-0 lines)
+    // reconverge before the group's next (warp-aligned) bar.sync: bar.sync from a diverged warp is
+    // undefined and released the barrier early (a race seen on 512^3 axis-0 lines)
     __syncwarp();
   }
 };
@@ -284,12 +325,22 @@ __device__ __forceinline__ void pass_compute(double (&xr)[C::R], double (&xi)[C:
     // Twiddles w^r, w = e^{2 pi i (v mod NS) / (NS RS)}: exact table values at the anchors r = 1 (mod 8),
     // the rest by the chain w^r = w^{r-1} w (<= 7 roundings from an anchor).  A load costs the L1 data
     // pipe 4 cycles per warp (tools/l1_probe.cu) while a complex multiply costs the FP64 pipe 2.
-    const double2 *twp = tw + TwOff<C::N, C::R, NS>::value + (v % NS);
-    const double2 w1 = __ldg(&twp[0]);
     double pr = 1.0, pim = 0.0;
+    double2 w1;
+    const double2 *twp;
+    if constexpr (C::TWS) {
+      twp = tw_smem_base(C::TW_OFF) + TwOff<C::N, C::R, NS>::value + (v % NS);
+    } else {
+      twp = tw + TwOff<C::N, C::R, NS>::value + (v % NS);
+      w1 = __ldg(&twp[0]);
+    }
 #pragma unroll
     for (int r = 1; r < RS; ++r) {
-      if (r % 8 == 1) {
+      if constexpr (C::TWS) {  // every twiddle from the SMEM table
+        const double2 wa = twp[(r - 1) * NS];
+        pr = wa.x;
+        pim = wa.y;
+      } else if (r % 8 == 1) {
         const double2 wa = r == 1 ? w1 : __ldg(&twp[(r - 1) * NS]);
         pr = wa.x;
         pim = wa.y;
@@ -387,10 +438,11 @@ struct Ctx {
     ring.base = smem;
     ring.full = reinterpret_cast<uint64_t *>(smem + C::NSTAGE * C::STAGE_BYTES);
     ring.empty = ring.full + C::NSTAGE;
+    ring.cnt = reinterpret_cast<unsigned *>(ring.empty + C::NSTAGE);
     ring.gv = ax.v;
     ring.gu = ax.ub;
     ring.r = ax.r;
-    ring.gph = ax.phivb;
+    ring.gph = ax.phivc;
     ring.k0 = ax.k0;
     char *gb = smem + C::HDR_BYTES + grp * C::GROUP_BYTES;
     buf = gb;
@@ -405,7 +457,7 @@ struct Ctx {
   // the others read bstart from global: their register budget has no room for the extra live state)
   __device__ static __forceinline__ int *binfo() {
     extern __shared__ __align__(128) char smem_raw[];
-    return reinterpret_cast<int *>(smem_raw + ((C::RING_BYTES + 127) / 128) * 128);
+    return reinterpret_cast<int *>(smem_raw + C::BINFO_OFF);
   }
   __device__ __forceinline__ void rows_of(const int *__restrict__ bstart, int q, int m, int &j0, int &cnt) const {
     if constexpr (C::STAGED) {
@@ -420,12 +472,17 @@ struct Ctx {
   // Ring set-up: barriers initialised and the first NSTAGE terms in flight before anyone waits; the
   // row-range table of the bins binof(vt, q) filled.
   template <class BinOf>
-  __device__ __forceinline__ void start(const int *__restrict__ bstart, BinOf binof) {
+  __device__ __forceinline__ void start(const int *__restrict__ bstart, const double2 *__restrict__ tw, BinOf binof) {
+    if constexpr (C::TWS) {
+      extern __shared__ __align__(128) char smem_raw[];
+      double2 *t = reinterpret_cast<double2 *>(smem_raw + C::TW_OFF);
+      for (int i = threadIdx.x; i < TwTotal<C::N, C::R>::value; i += C::NT) t[i] = __ldg(&tw[i]);
+    }
     if constexpr (C::STAGED) {
       if (threadIdx.x == 0) {
         for (int s = 0; s < C::NSTAGE; ++s) {
           mbar_init(&ring.full[s], 1);
-          mbar_init(&ring.empty[s], C::GPC);
+          ring.cnt[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (long long q = 0; q < C::NSTAGE && q < ring.total; ++q) ring.issue(q);
@@ -515,7 +572,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C> cx(smem_raw, ax, nlines);
-  cx.start(ax.bstart, [](int vt_, int q) { return q < R / 2 ? out_pos<C>(vt_, fwd_reg_of_bin<C>(q)) : C::N / 2; });
+  cx.start(ax.bstart, ax.tw, [](int vt_, int q) { return q < R / 2 ? out_pos<C>(vt_, fwd_reg_of_bin<C>(q)) : C::N / 2; });
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
   // degrees [0, kin) of W V are applied inside the term loop from the ring (KPT per term), the rest here
@@ -546,7 +603,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       for (int r = 0; r < R; ++r) {
         const int k = vt + r * TPL;
         a.set(r, av[r]);
-        if (r * TPL < K0MAX && k < k0) cx.alow[k * LG + line] = av[r];
+        if (r * TPL < K0MAX && k < K0MAX) cx.alow[k * LG + line] = k < k0 ? av[r] : 0.0;  // zero pad: W V pairs
       }
     }
 
@@ -574,17 +631,18 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
       if constexpr (C::VST) {  // A4 for degrees l KPT .. l KPT + KPT - 1 (rows of W V staged with the term)
-        const double *ph = cx.ring.ph(seq);
+        static_assert(C::KPT == 2, "W V chunks are read as double2 pairs");
+        const double2 *ph = reinterpret_cast<const double2 *>(cx.ring.ph(seq));
+        const int kb = l * C::KPT;
+        if (kb < k0) {  // chunk layout [m][c][kk]; degree kb + 1 >= k0 is zero-padded (alow padded too)
+          const double a0 = cx.alow[kb * LG + line], a1 = cx.alow[(kb + 1) * LG + line];
 #pragma unroll
-        for (int kk = 0; kk < C::KPT; ++kk) {
-          const int k = l * C::KPT + kk;
-          if (k < k0) {
-            const double ak = cx.alow[k * LG + line];
+          for (int q = 0; q < NB; ++q)
 #pragma unroll
-            for (int q = 0; q < NB; ++q)
-#pragma unroll
-              for (int c = 0; c < MAXR; ++c) y[q][c] = fma(ph[(kk * MAXR + c) * NBINS + m[q]], ak, y[q][c]);
-          }
+            for (int c = 0; c < MAXR; ++c) {
+              const double2 pp = ph[m[q] * MAXR + c];
+              y[q][c] = fma(pp.x, a0, fma(pp.y, a1, y[q][c]));
+            }
         }
       }
       double xr[R], xi[R];
@@ -635,7 +693,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C> cx(smem_raw, ax, nlines);
-  cx.start(ax.bstart, [](int vt_, int q) { return q < R / 2 ? vt_ + q * TPL : C::N / 2; });
+  cx.start(ax.bstart, ax.tw, [](int vt_, int q) { return q < R / 2 ? vt_ + q * TPL : C::N / 2; });
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
   // degrees [0, kin) of (W V)^T y are formed inside the term loop from the ring (KPT per term), the rest
@@ -714,7 +772,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       double pv[C::VST ? C::KPT : 1];  // partial (W V)^T y for degrees l KPT + kk (VST)
 #pragma unroll
       for (int kk = 0; kk < (C::VST ? C::KPT : 1); ++kk) pv[kk] = 0.0;
-      const double *ph = C::VST ? cx.ring.ph(seq) : nullptr;
+      const double2 *ph = reinterpret_cast<const double2 *>(C::VST ? cx.ring.ph(seq) : nullptr);
       const int kb = l * C::KPT;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -728,9 +786,11 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
             xr[r] = fma(uu.x, yv, xr[r]);
             xi[r] = fma(uu.y, yv, xi[r]);
             if constexpr (C::VST) {
-#pragma unroll
-              for (int kk = 0; kk < C::KPT; ++kk)
-                if (kb + kk < k0) pv[kk] = fma(ph[(kk * MAXR + c) * NBINS + m[r]], yv, pv[kk]);
+              if (kb < k0) {
+                const double2 pp = ph[m[r] * MAXR + c];
+                pv[0] = fma(pp.x, yv, pv[0]);
+                pv[1] = fma(pp.y, yv, pv[1]);
+              }
             }
           }
         }

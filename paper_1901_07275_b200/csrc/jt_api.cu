@@ -31,7 +31,7 @@ jt_status fail(jt_status s, const std::string &msg) {
 
 struct AxisDevBuf {
   double2 *ub = nullptr, *v = nullptr, *tw = nullptr;
-  double *phivb = nullptr;
+  double *phivb = nullptr, *phivc = nullptr;
   int *bstart = nullptr;
   int maxr = 0;  // row slots per bin in ub / phivb (template MAXR of the kernels)
 };
@@ -77,6 +77,7 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
   ax.v = p->dev[axis].v;
   ax.ub = p->dev[axis].ub;
   ax.phivb = p->dev[axis].phivb;
+  ax.phivc = p->dev[axis].phivc;
   ax.bstart = p->dev[axis].bstart;
   ax.tw = p->dev[axis].tw;
   return ax;
@@ -86,15 +87,20 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
 // (16x16, 32x16, 32x32), two for 2048 and 4096 (32x32x2, 32x32x4); see DESIGN.md "Kernels".
 // MAXR = 4 (more than two nodes in some bin: only for (a, b) near the ends of (-1, 1)) always uses
 // radix 16, whose accumulators fit in registers.
+#ifndef JT_R512
+#define JT_R512 32
+#endif
 template <int N, int MAXR>
 constexpr int radix_for() {
-  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : 32)));
+  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : 32))));
 }
-int radix_of(int64_t N, int maxr) { return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : 32))); }
+int radix_of(int64_t N, int maxr) {
+  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : 32))));
+}
 
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
 template <class C>
-jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
+jt_status launch_cfg(const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
                      const jtk::Layout &lay, cudaStream_t s) {
   const size_t smem = C::smem_bytes();
   const long long lines_per_batch = (long long)C::GPC * C::LG;
@@ -105,7 +111,7 @@ jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, dou
   JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const unsigned grid = (unsigned)std::min<long long>(batches, sms);
   const bool split = lay.in_cs != ax.n || lay.out_cs != ax.n;
-  if (inverse) {
+  if constexpr (C::INV) {
     auto kern = split ? jtk::inv_axis_kernel<C, true> : jtk::inv_axis_kernel<C, false>;
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay);
@@ -118,11 +124,18 @@ jt_status launch_cfg(bool inverse, const jtk::AxisDev &ax, const double *in, dou
   return JT_OK;
 }
 
+template <int N, int MAXR>
+jt_status launch_nm(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
+                    const jtk::Layout &lay, cudaStream_t s) {
+  if (inverse) return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, true>>(ax, in, out, nlines, lay, s);
+  return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, false>>(ax, in, out, nlines, lay, s);
+}
+
 template <int N>
 jt_status launch_n(bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
                    const jtk::Layout &lay, cudaStream_t s) {
-  if (maxr <= 2) return launch_cfg<jtk::Cfg<N, radix_for<N, 2>(), 2>>(inverse, ax, in, out, nlines, lay, s);
-  return launch_cfg<jtk::Cfg<N, radix_for<N, 4>(), 4>>(inverse, ax, in, out, nlines, lay, s);
+  if (maxr <= 2) return launch_nm<N, 2>(inverse, ax, in, out, nlines, lay, s);
+  return launch_nm<N, 4>(inverse, ax, in, out, nlines, lay, s);
 }
 
 // One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
@@ -168,6 +181,7 @@ void free_device(jt_plan_s *p) {
     cudaFree(p->dev[i].v);
     cudaFree(p->dev[i].tw);
     cudaFree(p->dev[i].phivb);
+    cudaFree(p->dev[i].phivc);
     cudaFree(p->dev[i].bstart);
     p->dev[i] = AxisDevBuf();
   }
@@ -190,6 +204,8 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   p->dev[axis].maxr = MAXR;
   std::vector<double2> ub((size_t)r * nbins * MAXR, make_double2(0.0, 0.0)), v((size_t)r * N), tw(N);
   std::vector<double> phivb((size_t)std::max(k0, 1) * nbins * MAXR, 0.0);
+  const int nchunk = std::max((k0 + 1) / 2, 1);
+  std::vector<double> phivc((size_t)nchunk * nbins * MAXR * 2, 0.0);
   for (int64_t m = 0; m < nbins; ++m) {
     for (int c = 0; c < h.bstart[m + 1] - h.bstart[m]; ++c) {
       const int64_t j = h.bstart[m] + c;
@@ -197,7 +213,10 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
         const jt::cd z = h.u[(size_t)j * r + l];
         ub[((size_t)l * MAXR + c) * nbins + m] = make_double2(z.real(), z.imag());
       }
-      for (int k = 0; k < k0; ++k) phivb[((size_t)k * MAXR + c) * nbins + m] = h.phiv[(size_t)j * k0 + k];
+      for (int k = 0; k < k0; ++k) {
+        phivb[((size_t)k * MAXR + c) * nbins + m] = h.phiv[(size_t)j * k0 + k];
+        phivc[(((size_t)(k / 2) * nbins + m) * MAXR + c) * 2 + (k % 2)] = h.phiv[(size_t)j * k0 + k];
+      }
     }
   }
   for (int l = 0; l < r; ++l) {
@@ -229,6 +248,7 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   if ((s = upload(&p->dev[axis].v, v.data(), v.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].tw, tw.data(), tw.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].phivb, phivb.data(), phivb.size())) != JT_OK) return s;
+  if ((s = upload(&p->dev[axis].phivc, phivc.data(), phivc.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].bstart, h.bstart.data(), h.bstart.size())) != JT_OK) return s;
   return JT_OK;
 }
