@@ -62,6 +62,8 @@ struct jt_plan_s {
   AxisDevBuf dev[3];
   int64_t total = 0;
   double *stage_in = nullptr, *stage_out = nullptr;  // for the *_host entry points
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;      // their copy streams
+  cudaEvent_t ev[2 * 16 + 2] = {};                     // and events
 };
 
 namespace {
@@ -141,10 +143,12 @@ jt_status launch_n(bool inverse, int maxr, const jtk::AxisDev &ax, const double 
 // One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
 // layout of the slab all-to-all for the input / output.
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
-                      long long inner, cudaStream_t s, int in_split = 1, int out_split = 1) {
+                      long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
+                      long long nlines_only = -1) {
   jtk::AxisDev ax = axis_dev(p, axis);
   const int maxr = p->dev[axis].maxr;
-  const long long nlines = outer * inner;
+  // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
+  const long long nlines = nlines_only >= 0 ? nlines_only : outer * inner;
   const jtk::Layout lay{outer, inner, (int)(p->n[axis] / in_split), (int)(p->n[axis] / out_split)};
   switch (ax.N) {
     case 16: return launch_n<16>(inverse, maxr, ax, in, out, nlines, lay, s);
@@ -188,6 +192,10 @@ void free_device(jt_plan_s *p) {
   cudaFree(p->stage_in);
   cudaFree(p->stage_out);
   p->stage_in = p->stage_out = nullptr;
+  for (auto &e : p->ev)
+    if (e) cudaEventDestroy(e), e = nullptr;
+  if (p->s_h2d) cudaStreamDestroy(p->s_h2d), p->s_h2d = nullptr;
+  if (p->s_d2h) cudaStreamDestroy(p->s_d2h), p->s_d2h = nullptr;
 }
 
 jt_status upload_axis(jt_plan_s *p, int axis) {
@@ -289,6 +297,11 @@ jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *
   return JT_OK;
 }
 
+// Host-buffer transform, pipelined (DESIGN.md §10 "e2e"): the input is copied in KC row chunks of axis 0
+// on a copy stream while the axis passes d-1 .. 1 run on each arrived chunk (their lines lie inside the
+// chunk); the axis-0 pass then runs in KC column blocks, each copied back (a pitched 2D copy) on a second
+// copy stream while the next block computes.  Every line runs the same kernel code as in jt_forward /
+// jt_inverse, so the results are bitwise identical to the device path.
 jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double *out_h, cudaStream_t s) {
   jt_status st = check_device_plan(p);
   if (st != JT_OK) return st;
@@ -298,10 +311,57 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
   if (!p->stage_in) {
     if (cudaMalloc((void **)&p->stage_in, bytes) != cudaSuccess) return fail(JT_ERR_ALLOC, "staging cudaMalloc");
     if (cudaMalloc((void **)&p->stage_out, bytes) != cudaSuccess) return fail(JT_ERR_ALLOC, "staging cudaMalloc");
+    JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+    JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+    for (auto &e : p->ev) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in, in_h, bytes, cudaMemcpyHostToDevice, s));
-  if ((st = transform(p, inverse, p->stage_in, p->stage_out, s)) != JT_OK) return st;
-  JT_CUDA_TRY(cudaMemcpyAsync(out_h, p->stage_out, bytes, cudaMemcpyDeviceToHost, s));
+  const int d = p->d;
+  const long long n0 = p->n[0];
+  const long long row = p->total / n0;  // elements per axis-0 index (the axis-0 pass's line count)
+  const int KC = (d == 1) ? 1 : (int)std::min<long long>(8, n0);
+  cudaEvent_t *ev_in = p->ev, *ev_out = p->ev + 16, ev_start = p->ev[32], ev_done = p->ev[33];
+  // the copy streams start after all prior work on s (the caller's ordering)
+  JT_CUDA_TRY(cudaEventRecord(ev_start, s));
+  JT_CUDA_TRY(cudaStreamWaitEvent(p->s_h2d, ev_start, 0));
+  JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_start, 0));
+  if (d == 1) {
+    JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in, in_h, bytes, cudaMemcpyHostToDevice, s));
+    if ((st = transform(p, inverse, p->stage_in, p->stage_out, s)) != JT_OK) return st;
+    JT_CUDA_TRY(cudaMemcpyAsync(out_h, p->stage_out, bytes, cudaMemcpyDeviceToHost, s));
+    JT_CUDA_TRY(cudaStreamSynchronize(s));
+    return JT_OK;
+  }
+  // phase 1: row chunks of axis 0
+  for (int c = 0; c < KC; ++c) {
+    const long long r0 = n0 * c / KC, r1 = n0 * (c + 1) / KC;
+    const size_t off = (size_t)(r0 * row), cnt = (size_t)((r1 - r0) * row);
+    JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in + off, in_h + off, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                p->s_h2d));
+    JT_CUDA_TRY(cudaEventRecord(ev_in[c], p->s_h2d));
+    JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[c], 0));
+    const double *src = p->stage_in + off;
+    for (int axis = d - 1; axis >= 1; --axis) {
+      long long outer = r1 - r0, inner = 1;
+      for (int i = 1; i < axis; ++i) outer *= p->n[i];
+      for (int i = axis + 1; i < d; ++i) inner *= p->n[i];
+      if ((st = launch_axis(p, axis, inverse, src, p->stage_out + off, outer, inner, s)) != JT_OK) return st;
+      src = p->stage_out + off;
+    }
+  }
+  // phase 2: axis-0 pass in column blocks, each copied back while the next computes
+  for (int c = 0; c < KC; ++c) {
+    const long long c0 = row * c / KC, c1 = row * (c + 1) / KC;
+    if (c1 == c0) continue;
+    if ((st = launch_axis(p, 0, inverse, p->stage_out + c0, p->stage_out + c0, 1, row, s, 1, 1, c1 - c0)) != JT_OK)
+      return st;
+    JT_CUDA_TRY(cudaEventRecord(ev_out[c], s));
+    JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[c], 0));
+    JT_CUDA_TRY(cudaMemcpy2DAsync(out_h + c0, (size_t)row * sizeof(double), p->stage_out + c0,
+                                  (size_t)row * sizeof(double), (size_t)(c1 - c0) * sizeof(double), (size_t)n0,
+                                  cudaMemcpyDeviceToHost, p->s_d2h));
+  }
+  JT_CUDA_TRY(cudaEventRecord(ev_done, p->s_d2h));
+  JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
   JT_CUDA_TRY(cudaStreamSynchronize(s));
   return JT_OK;
 }

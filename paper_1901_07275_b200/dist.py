@@ -153,6 +153,13 @@ class SlabPlan:
         self._axis(1, True, self._recv, out, n0 // G, r, G, 1)
         return out
 
+    def forward_host(self, x_host, y_host, x_dev, y_dev):
+        """End-to-end forward of this rank's x-slab: pinned host x-slab -> device -> transform -> host y-slab."""
+        x_dev.copy_(x_host, non_blocking=True)
+        self.forward(x_dev, y_dev)
+        y_host.copy_(y_dev, non_blocking=True)
+        return y_host
+
     def make_forward_step(self, x):
         """Closure running one forward transform of the resident x-slab into a preallocated y-slab."""
         import torch
