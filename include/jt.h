@@ -74,6 +74,31 @@ jt_status jt_default_opts(jt_opts *o);
 jt_status jt_plan(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
                   double eps, const jt_opts *opts);
 
+/* Kinds of modified Jacobi functions (PAPER.md:111-122 eq:modifiedjac, eq:modifiedjac2). */
+enum { JT_KIND_P = 0 /* P~ (first kind) */, JT_KIND_Q = 1 /* Q~ (second kind) */ };
+
+/* Extended plan:
+ *   points  NULL, or d host pointers; points[i] == NULL selects the UNIFORM transform on axis i (Gauss-Jacobi
+ *           nodes, rows weighted by sqrt(w_j), as jt_plan), otherwise points[i] holds n[i] NONUNIFORM points
+ *           t_j in (0, pi), non-decreasing, and axis i's matrix is J itself (W = I, "the nonuniform forward
+ *           Jacobi transform does not require trigonometric Gauss-Jacobi quadrature nodes and weights",
+ *           PAPER.md:491; the same low-rank (.) DFT factorisation applies).  Points
+ *           clustered so that more than 4 fall into one FFT bin raise the FFT length (up to 4096), else
+ *           JT_ERR_NUMERIC.  The points are copied; the caller keeps ownership.
+ *   kind    JT_KIND_P: expansions in P~_k; JT_KIND_Q: in Q~_k ("the transform for Q~ is similar",
+ *           PAPER.md:457, 646; Q~ normalised as in DESIGN.md reading R8).
+ * Only uniform first-kind plans are orthogonal: jt_inverse / jt_inverse_host refuse the others (JT_ERR_ARG;
+ * the nonuniform inverse is an open problem); jt_adjoint applies the transpose for any plan. */
+jt_status jt_plan_ex(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
+                     const double *const points[], int kind, double eps, const jt_opts *opts);
+
+/* Transpose transform coeffs = (M_0^T (x) ... (x) M_{d-1}^T) values for any plan (M_i axis i's matrix); equal
+ * to jt_inverse for uniform first-kind plans.  Device pointers, same rules as jt_forward. */
+jt_status jt_adjoint(jt_plan_t p, const double *values, double *coeffs, void *cuda_stream);
+
+/* Whether axis `axis` is uniform (1) or nonuniform (0), and its kind (JT_KIND_P / JT_KIND_Q). */
+jt_status jt_plan_kind(jt_plan_t p, int axis, int *uniform, int *kind);
+
 /* Forward transform, device pointers (fp64, C-order, prod(n) elements each, 16-byte aligned).
  * coeffs is read-only; values is written.  coeffs == values is allowed (in place); partial overlap
  * is JT_ERR_ARG.  Runs d fused axis passes. */

@@ -267,3 +267,121 @@ def kron_matrix(shape, a, b) -> np.ndarray:
     for ax, n in enumerate(shape):
         K = np.kron(K, phi(int(n), a[ax], b[ax]))
     return K
+
+
+# ---------------------------------------------------------------------------------------------------
+# SURVEY.md §8(f) NEXT-1 (nonuniform forward) and NEXT-3 (second-kind Q~ transforms): the same plain
+# definitions at arbitrary angles.  PAPER.md:491 ("the nonuniform forward Jacobi transform does not require
+# trigonometric Gauss-Jacobi quadrature nodes and weights": the matrix is J itself, W = I), PAPER.md:457 and
+# 646 ("the transform for Q~ is similar"), eq:modifiedjac / eq:modifiedjac2.
+# ---------------------------------------------------------------------------------------------------
+def _trig_scale(t, a: float, b: float):
+    """sqrt(2^{a+b+1}) sin(t/2)^{a+1/2} cos(t/2)^{b+1/2} in longdouble (eq:modifiedjac, PAPER.md:111-116)."""
+    t = np.asarray(t, dtype=LD)
+    aa, bb = _ld(a), _ld(b)
+    return np.sqrt(LD(2) ** (aa + bb + 1)) * np.sin(t / 2) ** (aa + LD(0.5)) * np.cos(t / 2) ** (bb + LD(0.5))
+
+
+def cauchy_h0(t, a: float, b: float):
+    """H_0(x) = PV int_{-1}^{1} w(y) / (x - y) dy, w(y) = (1-y)^a (1+y)^b, x = cos t, for each angle (float64
+    array in, longdouble out).  The principal value written as the plain integral of (w(y) - w(x))/(x - y)
+    (a removable singularity at y = x) plus w(x) log((1+x)/(1-x)), by mpmath tanh-sinh quadrature at 60 digits
+    split at y = x, in the variables 1 + y and 1 - y (exact near the singular ends).  (reading R8; the definition of the second-kind functions via the Cauchy
+    transform.)"""
+    out = np.empty(len(t), dtype=LD)
+    with mpmath.workdps(60):  # 60 digits: the (w(y) - w(x)) / (x - y) cancellation at nodes next to y = x
+        A, B = mpmath.mpf(a), mpmath.mpf(b)
+        for j, tj in enumerate(np.asarray(t, dtype=np.float64)):
+            th = mpmath.mpf(float(tj))
+            omx = 2 * mpmath.sin(th / 2) ** 2      # 1 - x, no cancellation
+            opx = 2 * mpmath.cos(th / 2) ** 2      # 1 + x
+            x = 1 - omx
+            wx = omx ** A * opx ** B
+
+            # substitute s = 1 + y on [-1, x] and s = 1 - y on [x, 1] so that the endpoint factors (1 +- y)
+            # are the quadrature variable itself (exact near the singular ends of w)
+            def f_lo(s_):  # y = -1 + s
+                return ((2 - s_) ** A * s_ ** B - wx) / (opx - s_)
+
+            def f_hi(s_):  # y = 1 - s
+                return (s_ ** A * (2 - s_) ** B - wx) / (s_ - omx)
+
+            def integral(f, e, c):
+                # int_0^c f(s) ds with f ~ s^e at 0: for e < 0 substitute s = u^p, p = 1/(1+e), which makes the
+                # integrand bounded (a truncated tanh-sinh tail of s^e would cost c_min^{1+e}, ~1e-6 at e = -0.9)
+                if e >= 0:
+                    return mpmath.quad(f, [0, c])
+                p_ = 1 / (1 + e)
+                return mpmath.quad(lambda u: f(u ** p_) * p_ * u ** (p_ - 1), [0, c ** (1 + e)])
+            v = integral(f_lo, B, opx) + integral(f_hi, A, omx) + wx * mpmath.log(opx / omx)
+            out[j] = _ld(v)
+    return out
+
+
+def modified_q_all(t, kmax: int, a: float, b: float):
+    """Q~_k(t) for k = 0..kmax (rows) at the angles t (columns), longdouble, by the definition of reading R8:
+        Q~_k(t) = -sqrt(sin t / w(x)) H_k(x) / pi,  H_k(x) = PV int w(y) p_k(y) / (x - y) dy,
+    with H_0 from `cauchy_h0` and the three-term recurrence of the p_k carried over to H_k: for k >= 1,
+    H_{k+1} = ((x - alpha_k) H_k - beta_k H_{k-1}) / beta_{k+1}, and H_1 = ((x - alpha_0) H_0 - sqrt(mu0)) / beta_1
+    (the k = 0 moment term: int w p_0 = sqrt(mu0); it vanishes for k >= 1 by orthogonality)."""
+    t = np.asarray(t, dtype=LD)
+    alpha, beta = recurrence_coefficients(kmax + 1, a, b)
+    H = np.zeros((kmax + 1,) + t.shape, dtype=LD)
+    H[0] = cauchy_h0(t.astype(np.float64), a, b) / np.sqrt(mu0(a, b))   # H for p_0 = mu0^{-1/2}
+    x_minus = _x_minus_alpha_factory(t)
+    if kmax >= 1:
+        H[1] = (x_minus(alpha[0]) * H[0] - np.sqrt(mu0(a, b))) / beta[1]
+    for k in range(1, kmax):
+        H[k + 1] = (x_minus(alpha[k]) * H[k] - beta[k] * H[k - 1]) / beta[k + 1]
+    aa, bb = _ld(a), _ld(b)
+    w = (2 * np.sin(t / 2) ** 2) ** aa * (2 * np.cos(t / 2) ** 2) ** bb
+    return -np.sqrt(np.sin(t) / w) * H / LD(np.pi)
+
+
+def phi_points(t, n: int, a: float, b: float, kind: int = 0) -> np.ndarray:
+    """The m x n matrix J[j, k] = P~_k(t_j) (kind 0) or Q~_k(t_j) (kind 1) at arbitrary angles t_j in (0, pi)
+    (unweighted: the nonuniform transform's matrix).  longdouble entries rounded once."""
+    t = np.asarray(t, dtype=np.float64)
+    if kind == 0:
+        M = (_trig_scale(t, a, b)[None, :] * p_all(t, n - 1, a, b)).T
+    else:
+        M = modified_q_all(t, n - 1, a, b).T
+    return np.ascontiguousarray(M.astype(np.float64))
+
+
+@functools.lru_cache(maxsize=32)
+def phi_q_uniform(n: int, a: float, b: float) -> np.ndarray:
+    """Uniform second-kind matrix sqrt(w_j) Q~_k(t_j) at the Gauss-Jacobi nodes (rows weighted as W J_n)."""
+    t, _, w = gauss_jacobi(n, a, b)
+    M = np.sqrt(w)[:, None] * modified_q_all(t, n - 1, a, b).T
+    out = np.ascontiguousarray(M.astype(np.float64))
+    out.setflags(write=False)
+    return out
+
+
+def axis_matrix(n: int, a: float, b: float, points=None, kind: int = 0) -> np.ndarray:
+    """Axis matrix of a plan: uniform weighted (points None) or nonuniform unweighted; first or second kind."""
+    if points is None:
+        return phi(n, a, b) if kind == 0 else phi_q_uniform(n, a, b)
+    return phi_points(points, n, a, b, kind)
+
+
+def forward_ex(coeffs: np.ndarray, a, b, points=None, kind: int = 0) -> np.ndarray:
+    """values = (M_0 (x) ... (x) M_{d-1}) coeffs with the per-axis matrices of `axis_matrix`
+    (points: None, or one entry per axis, None = uniform)."""
+    X = np.asarray(coeffs, dtype=np.float64)
+    a, b = _params(X.shape, a, b)
+    for ax in range(X.ndim):
+        pts = None if points is None else points[ax]
+        X = _mode_product(axis_matrix(X.shape[ax], a[ax], b[ax], pts, kind), X, ax)
+    return np.ascontiguousarray(X)
+
+
+def adjoint_ex(values: np.ndarray, a, b, points=None, kind: int = 0) -> np.ndarray:
+    """coeffs = (M_0^T (x) ... (x) M_{d-1}^T) values (the transpose; the inverse only when orthogonal)."""
+    X = np.asarray(values, dtype=np.float64)
+    a, b = _params(X.shape, a, b)
+    for ax in range(X.ndim):
+        pts = None if points is None else points[ax]
+        X = _mode_product(axis_matrix(X.shape[ax], a[ax], b[ax], pts, kind).T, X, ax)
+    return np.ascontiguousarray(X)

@@ -26,11 +26,12 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 JT_OK, JT_ERR_ARG, JT_ERR_DOMAIN, JT_ERR_NUMERIC, JT_ERR_ALLOC, JT_ERR_CUDA, JT_ERR_NCCL = range(7)
+JT_KIND_P, JT_KIND_Q = 0, 1
 _STATUS = {0: "JT_OK", 1: "JT_ERR_ARG", 2: "JT_ERR_DOMAIN", 3: "JT_ERR_NUMERIC", 4: "JT_ERR_ALLOC",
            5: "JT_ERR_CUDA", 6: "JT_ERR_NCCL"}
 
 # Every symbol declared in include/jt.h and include/jt_debug.h (checked by tests/test_abi.py).
-EXPORTED = ["jt_default_opts", "jt_plan", "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
+EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_kind", "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
             "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_destroy", "jt_plan_rank", "jt_plan_info",
             "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_error", "jt_version",
             "jt_debug_modified_pq"]
@@ -53,7 +54,10 @@ _D = ctypes.POINTER(ctypes.c_double)
 _I64 = ctypes.POINTER(ctypes.c_int64)
 _lib.jt_default_opts.argtypes = [ctypes.POINTER(jt_opts)]
 _lib.jt_plan.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double, ctypes.POINTER(jt_opts)]
-for _f in ("jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host"):
+_lib.jt_plan_ex.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_void_p, ctypes.c_int,
+                            ctypes.c_double, ctypes.POINTER(jt_opts)]
+_lib.jt_plan_kind.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+for _f in ("jt_forward", "jt_inverse", "jt_adjoint", "jt_forward_host", "jt_inverse_host"):
     getattr(_lib, _f).argtypes = [_P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 for _f in ("jt_forward_axis", "jt_inverse_axis"):
     getattr(_lib, _f).argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
@@ -112,8 +116,12 @@ def jt_default_opts() -> jt_opts:
 
 
 def jt_plan(n, a, b, eps: float = 1e-12, seed: int = 0, k0: int = 27, rmax_init: int = 0, q: int = 3,
-            sweeps: int = 2, device: int = -1) -> int:
-    """Build a plan (C: jt_plan).  device=-1: current CUDA device; device=-2: host-only plan."""
+            sweeps: int = 2, device: int = -1, points=None, kind: int = JT_KIND_P) -> int:
+    """Build a plan (C: jt_plan, or jt_plan_ex when `points` / `kind` are given).
+
+    device=-1: current CUDA device; device=-2: host-only plan.  points: None (uniform) or a sequence of d
+    entries, each None (uniform axis) or n[i] nonuniform points in (0, pi), non-decreasing.  kind: JT_KIND_P
+    (P~ expansions) or JT_KIND_Q (Q~ expansions)."""
     n = [int(v) for v in np.atleast_1d(n)]
     d = len(n)
     a = np.broadcast_to(np.asarray(a, dtype=np.float64), (d,)).copy()
@@ -121,8 +129,26 @@ def jt_plan(n, a, b, eps: float = 1e-12, seed: int = 0, k0: int = 27, rmax_init:
     o = jt_default_opts()
     o.seed, o.k0, o.rmax_init, o.q, o.sweeps, o.device = seed, k0, rmax_init, q, sweeps, device
     h = _P()
-    _check(_lib.jt_plan(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D), b.ctypes.data_as(_D),
-                        float(eps), ctypes.byref(o)), "jt_plan")
+    if points is None and kind == JT_KIND_P:
+        _check(_lib.jt_plan(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D),
+                            b.ctypes.data_as(_D), float(eps), ctypes.byref(o)), "jt_plan")
+        return h.value
+    keep = []
+    ptrs = (ctypes.c_void_p * d)()
+    if points is not None:
+        if len(points) != d:
+            raise ValueError("points needs one entry per axis")
+        for i, pts in enumerate(points):
+            if pts is None:
+                continue
+            arr = np.ascontiguousarray(pts, dtype=np.float64)
+            if arr.shape != (n[i],):
+                raise ValueError(f"axis {i}: expected {n[i]} points")
+            keep.append(arr)
+            ptrs[i] = arr.ctypes.data
+    _check(_lib.jt_plan_ex(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D),
+                           b.ctypes.data_as(_D), ctypes.cast(ptrs, ctypes.c_void_p) if points is not None else None,
+                           int(kind), float(eps), ctypes.byref(o)), "jt_plan_ex")
     return h.value
 
 
@@ -132,6 +158,17 @@ def jt_forward(plan: int, coeffs, values, stream=None):
 
 def jt_inverse(plan: int, values, coeffs, stream=None):
     _check(_lib.jt_inverse(plan, _ptr(values), _ptr(coeffs), _stream_handle(stream)), "jt_inverse")
+
+
+def jt_adjoint(plan: int, values, coeffs, stream=None):
+    _check(_lib.jt_adjoint(plan, _ptr(values), _ptr(coeffs), _stream_handle(stream)), "jt_adjoint")
+
+
+def jt_plan_kind(plan: int, axis: int):
+    """(uniform: bool, kind: int) of axis `axis`."""
+    u, k = ctypes.c_int(), ctypes.c_int()
+    _check(_lib.jt_plan_kind(plan, axis, ctypes.byref(u), ctypes.byref(k)), "jt_plan_kind")
+    return bool(u.value), k.value
 
 
 def jt_forward_host(plan: int, coeffs_host: np.ndarray, values_host: np.ndarray, stream=None):
@@ -242,6 +279,14 @@ class Plan:
         out = self._out(values, out)
         jt_inverse(self.handle, values, out, stream)
         return out
+
+    def adjoint(self, values, out=None, stream=None):
+        out = self._out(values, out)
+        jt_adjoint(self.handle, values, out, stream)
+        return out
+
+    def kind(self, axis: int = 0):
+        return jt_plan_kind(self.handle, axis)
 
     def forward_host(self, coeffs: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
         coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)

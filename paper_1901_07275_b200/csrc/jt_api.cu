@@ -387,7 +387,13 @@ jt_status jt_default_opts(jt_opts *o) {
 
 jt_status jt_plan(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
                   const jt_opts *opts) {
+  return jt_plan_ex(out, d, n, a, b, nullptr, JT_KIND_P, eps, opts);
+}
+
+jt_status jt_plan_ex(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
+                     const double *const points[], int kind, double eps, const jt_opts *opts) {
   if (!out) return fail(JT_ERR_ARG, "null out");
+  if (kind != JT_KIND_P && kind != JT_KIND_Q) return fail(JT_ERR_ARG, "kind must be JT_KIND_P or JT_KIND_Q");
   *out = nullptr;
   if (d < 1 || d > 3) return fail(JT_ERR_ARG, "d must be 1, 2 or 3");
   if (!n || !a || !b) return fail(JT_ERR_ARG, "null n/a/b");
@@ -416,15 +422,20 @@ jt_status jt_plan(jt_plan_t *out, int d, const int64_t n[], const double a[], co
   try {
     for (int i = 0; i < d; ++i) {
       // identical axes share the host computation
+      const double *pts = points ? points[i] : nullptr;
       int same = -1;
-      for (int k = 0; k < i; ++k)
-        if (n[k] == n[i] && a[k] == a[i] && b[k] == b[i]) same = k;
+      for (int k = 0; k < i; ++k) {
+        const double *pk = points ? points[k] : nullptr;
+        const bool same_pts = (pk == nullptr && pts == nullptr) ||
+                              (pk && pts && n[k] == n[i] && std::memcmp(pk, pts, n[i] * sizeof(double)) == 0);
+        if (n[k] == n[i] && a[k] == a[i] && b[k] == b[i] && same_pts) same = k;
+      }
       if (same >= 0) {
         p->host[i] = p->host[same];
         continue;
       }
       std::string err;
-      jt_status s = jt::build_axis_host(p->host[i], n[i], a[i], b[i], eps, o, err);
+      jt_status s = jt::build_axis_host(p->host[i], n[i], a[i], b[i], eps, o, err, pts, kind);
       if (s != JT_OK) {
         delete p;
         return fail(s, "axis " + std::to_string(i) + ": " + err);
@@ -463,8 +474,30 @@ jt_status jt_forward(jt_plan_t p, const double *coeffs, double *values, void *st
   return transform(p, false, coeffs, values, (cudaStream_t)stream);
 }
 
+static jt_status check_orthogonal(jt_plan_t p) {
+  if (!p) return fail(JT_ERR_ARG, "null plan");
+  for (int i = 0; i < p->d; ++i)
+    if (!p->host[i].uniform || p->host[i].kind != JT_KIND_P)
+      return fail(JT_ERR_ARG, "jt_inverse needs a uniform first-kind plan (the nonuniform / second-kind matrix is not "
+                              "orthogonal, PAPER.md:509; jt_adjoint applies its transpose)");
+  return JT_OK;
+}
+
 jt_status jt_inverse(jt_plan_t p, const double *values, double *coeffs, void *stream) {
+  jt_status st = check_orthogonal(p);
+  if (st != JT_OK) return st;
   return transform(p, true, values, coeffs, (cudaStream_t)stream);
+}
+
+jt_status jt_adjoint(jt_plan_t p, const double *values, double *coeffs, void *stream) {
+  return transform(p, true, values, coeffs, (cudaStream_t)stream);
+}
+
+jt_status jt_plan_kind(jt_plan_t p, int axis, int *uniform, int *kind) {
+  if (!p || axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad args");
+  if (uniform) *uniform = p->host[axis].uniform ? 1 : 0;
+  if (kind) *kind = p->host[axis].kind;
+  return JT_OK;
 }
 
 jt_status jt_forward_host(jt_plan_t p, const double *coeffs_host, double *values_host, void *stream) {
@@ -472,6 +505,8 @@ jt_status jt_forward_host(jt_plan_t p, const double *coeffs_host, double *values
 }
 
 jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs_host, void *stream) {
+  jt_status st = check_orthogonal(p);
+  if (st != JT_OK) return st;
   return transform_host(p, true, values_host, coeffs_host, (cudaStream_t)stream);
 }
 

@@ -32,11 +32,15 @@ struct AxisHost {
   std::vector<int32_t> bins, bstart;
   std::vector<double> sigma;  // singular values of Algorithm 1's middle matrix (descending)
   int rmax_used = 0;
+  bool uniform = true;  // Gauss-Jacobi nodes, weighted rows (false: caller's points, unweighted)
+  int kind = 0;         // 0: P~ (first kind), 1: Q~ (second kind)
 };
 
 // Builds one axis's plan on the host.  Returns JT_OK or an error code with `err` filled.
+// points == nullptr: uniform (Gauss-Jacobi nodes); else n caller points in (0, pi), non-decreasing.
+// kind 0: P~, 1: Q~.
 jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double eps, const jt_opts &opts,
-                          std::string &err);
+                          std::string &err, const double *points = nullptr, int kind = 0);
 
 // Debug / test hook: P~_k(t) and Q~_k(t) (PAPER.md eq:modifiedjac, eq:modifiedjac2; reading R8 for Q~)
 // for k = 0..kmax at the angles t[0..nt-1], by the plan's own route (Cauchy transform h0 + recurrence).

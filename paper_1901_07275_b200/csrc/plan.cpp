@@ -574,33 +574,78 @@ static void algorithm1(const ZView &Z, int r, int q, int sweeps, std::mt19937_64
 }
 
 jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double eps, const jt_opts &opts,
-                          std::string &err) {
+                          std::string &err, const double *points, int kind) {
   ax = AxisHost();
   ax.n = n;
   ax.N = fft_length(n);
   ax.a = a;
   ax.b = b;
+  ax.kind = kind;
+  ax.uniform = points == nullptr;
   ax.k0 = (int)std::min<int64_t>(std::max(opts.k0, 0), n);
-  const int64_t N = ax.N;
   const int k0 = ax.k0;
   Recurrence R = make_recurrence(n + 1, a, b);
-  std::vector<ld> t, lam;
-  if (!gauss_jacobi_t(n, a, b, R, t, lam)) {
-    err = "Gauss-Jacobi Newton iteration did not converge";
-    return JT_ERR_NUMERIC;
+  // Row scale s_j of the entries s_j z_k(t_j) (z_k = p_k - i H_k / (pi w), see z_sweep):
+  //   uniform (Gauss-Jacobi nodes):  s_j = sqrt(lambda_j)  -> sqrt(w_j) (P~ + iQ~)_k(t_j)  (the weighted W J_n)
+  //   nonuniform (given points):     s_j = sqrt(w(x_j) sin t_j) -> (P~ + iQ~)_k(t_j)      (J_n itself, W = I:
+  //                                  "does not require ... quadrature nodes and weights")
+  std::vector<ld> t, scale(n);
+  if (ax.uniform) {
+    std::vector<ld> lam;
+    if (!gauss_jacobi_t(n, a, b, R, t, lam)) {
+      err = "Gauss-Jacobi Newton iteration did not converge";
+      return JT_ERR_NUMERIC;
+    }
+    for (int64_t j = 0; j < n; ++j) scale[j] = sqrtl(lam[j]);
+    ax.t.resize(n);
+    ax.w.resize(n);
+    for (int64_t j = 0; j < n; ++j) {
+      ax.t[j] = (double)t[j];
+      TForm tf(t[j]);
+      // w_j = lambda_j / (2^{a+b+1} sin^{2a+1}(t/2) cos^{2b+1}(t/2)) = lambda_j / (sx^{a+1/2} cx^{b+1/2})
+      ax.w[j] = (double)(lam[j] / (powl(tf.sx, (ld)a + 0.5L) * powl(tf.cx, (ld)b + 0.5L)));
+    }
+  } else {
+    t.resize(n);
+    ax.t.assign(points, points + n);
+    ax.w.assign(n, 1.0);
+    for (int64_t j = 0; j < n; ++j) {
+      if (!(points[j] > 0 && points[j] < 3.141592653589793) || (j > 0 && points[j] < points[j - 1])) {
+        err = "nonuniform points must lie in (0, pi) in non-decreasing order";
+        return JT_ERR_ARG;
+      }
+      t[j] = points[j];
+      TForm tf(t[j]);
+      scale[j] = sqrtl(powl(tf.sx, (ld)a) * powl(tf.cx, (ld)b) * sinl(t[j]));
+    }
   }
-  ax.t.resize(n);
-  ax.w.resize(n);
-  ax.bins.resize(n);
-  for (int64_t j = 0; j < n; ++j) {
-    ax.t[j] = (double)t[j];
-    TForm tf(t[j]);
-    // w_j = lambda_j / (2^{a+b+1} sin^{2a+1}(t/2) cos^{2b+1}(t/2)) = lambda_j / (sx^{a+1/2} cx^{b+1/2})
-    ax.w[j] = (double)(lam[j] / (powl(tf.sx, (ld)a + 0.5L) * powl(tf.cx, (ld)b + 0.5L)));
-    ax.bins[j] = (int32_t)nearbyintl(t[j] * (ld)N / (2 * PI_L));
+  // Bins m_j = [t_j N / 2 pi] (eq:B) hold at most 4 rows each (the kernels' MAXR).  Gauss-Jacobi
+  // nodes never exceed it.  Clustered nonuniform points are spread greedily to the next bins (m_j stays
+  // non-decreasing in j; the factorisation absorbs the larger residual t_j - 2 pi m_j / N as extra rank),
+  // displacing no point by more than 2 bins; if that fails the FFT length doubles (up to the kernels' 4096).
+  for (;;) {
+    ax.bins.assign(n, 0);
+    ax.bstart.assign(ax.N / 2 + 2, 0);
+    bool ok = true;
+    int32_t prev = 0;
+    for (int64_t j = 0; j < n && ok; ++j) {
+      const int32_t m0 = (int32_t)nearbyintl(t[j] * (ld)ax.N / (2 * PI_L));
+      int32_t m = std::max(m0, prev);
+      while (m <= ax.N / 2 && ax.bstart[m + 1] >= 4) ++m;
+      if (m > ax.N / 2 || m - m0 > 2) ok = false;
+      else {
+        ax.bins[j] = prev = m;
+        ax.bstart[m + 1]++;
+      }
+    }
+    if (ok) break;
+    if (ax.N >= 4096) {
+      err = "points too clustered: more than 4 per FFT bin within 2 bins even at FFT length 4096";
+      return JT_ERR_NUMERIC;
+    }
+    ax.N *= 2;
   }
-  ax.bstart.assign(N / 2 + 2, 0);
-  for (int64_t j = 0; j < n; ++j) ax.bstart[ax.bins[j] + 1]++;
+  const int64_t N = ax.N;
   for (int64_t m = 0; m < N / 2 + 1; ++m) ax.bstart[m + 1] += ax.bstart[m];
 
   // Entries: phiv (k < k0) and Z = W B (k >= k0), row by row in long double.
@@ -611,9 +656,14 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
   std::vector<cd> Z((size_t)n * std::max(nc, 0));
 #pragma omp parallel for schedule(dynamic, 4)
   for (int64_t j = 0; j < n; ++j) {
-    ld sl = sqrtl(lam[j]);
+    ld sl = scale[j];
     int64_t mj = ax.bins[j];
     z_sweep(R, t[j], a, b, n - 1, [&](int64_t k, ld zr, ld zi) {
+      if (kind == 1) {  // second kind: Q~ = Im z = Re(-i z) (NEXT-3, "the transform for Q~ is similar")
+        const ld tr = zr;
+        zr = zi;
+        zi = -tr;
+      }
       if (k < k0) {
         ax.phiv[(size_t)j * k0 + k] = (double)(sl * zr);
       } else {
