@@ -97,11 +97,12 @@ def cpu_oracle_rate(cfg, max_seconds: float = 30.0):
     fits the time bound, else a slab of it.  Returns (coefficients/s, sample description, threads)."""
     import oracle
     shape, a, b = cfg["n"], cfg["a"], cfg["b"]
+    pts, kind = si.config_points(cfg), cfg.get("kind", 0)
     for ax in range(len(shape)):  # Phi construction is the oracle's "fac"; not part of the apply rate
-        oracle.phi(shape[ax], a[ax], b[ax])
+        oracle.axis_matrix(shape[ax], a[ax], b[ax], None if pts is None else pts[ax], kind)
     x = si.gaussian(shape, seed=0)
     t0 = time.perf_counter()
-    oracle.forward(x, a, b)
+    oracle.forward_ex(x, a, b, pts, kind)
     dt = time.perf_counter() - t0
     threads = os.cpu_count()
     try:
@@ -119,8 +120,9 @@ def run_reference(args, cfg, rank: int):
         return
     import oracle
     shape, a, b = cfg["n"], cfg["a"], cfg["b"]
+    pts, kind = si.config_points(cfg), cfg.get("kind", 0)
     for ax in range(len(shape)):
-        oracle.phi(shape[ax], a[ax], b[ax])
+        oracle.axis_matrix(shape[ax], a[ax], b[ax], None if pts is None else pts[ax], kind)
     # Bounded sample per step (1/8 of the transform's work): the last d-1 axis passes on an x-slab of
     # n0/8 planes, and the axis-0 pass on the full-height block of the first n1/8 columns.  Both have the
     # exact per-point cost of the full transform's passes.
@@ -129,10 +131,10 @@ def run_reference(args, cfg, rank: int):
     xs = np.ascontiguousarray(x[:slab])
 
     def step():
-        y = oracle.forward_axes(xs, a, b, axes=list(range(len(shape) - 1, 0, -1)))
+        y = oracle.forward_axes(xs, a, b, axes=list(range(len(shape) - 1, 0, -1)), points=pts, kind=kind)
         # axis 0 on the full-height columns of the first slab/8 columns of axis 1 (bounded work)
         cols = np.ascontiguousarray(x[:, : max(1, shape[1] // 8)])
-        oracle.forward_axes(cols, a, b, axes=[0])
+        oracle.forward_axes(cols, a, b, axes=[0], points=pts, kind=kind)
         return y
 
     pts_step = xs.size + (x[:, : max(1, shape[1] // 8)].size if len(shape) > 1 else 0)
@@ -159,7 +161,9 @@ def run_reference(args, cfg, rank: int):
 
 
 def config_block(args, cfg, ranks):
-    return {"workload": f"{args.config}: {'x'.join(map(str, cfg['n']))} uniform forward, (a,b)="
+    kindtxt = ("nonuniform (random points)" if cfg.get("points") else "uniform") + (
+        " second-kind Q~" if cfg.get("kind", 0) == 1 else "")
+    return {"workload": f"{args.config}: {'x'.join(map(str, cfg['n']))} {kindtxt} forward, (a,b)="
                         f"{list(zip(cfg['a'], cfg['b']))}, eps={cfg['eps']}",
             "model": "none (transform)", "global_batch": 1, "seq_len": int(np.prod(cfg["n"])),
             "ranks_per_axis": ranks, "k0": K0, "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
@@ -199,7 +203,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     if world == 1:
-        plan = jt.Plan(shape, a, b, eps)
+        plan = jt.Plan(shape, a, b, eps, points=si.config_points(cfg), kind=cfg.get("kind", 0))
         ranks = [plan.rank(i) for i in range(d)]
         x = torch.from_numpy(si.gaussian(shape, seed=0)).cuda()
         y = torch.empty_like(x)

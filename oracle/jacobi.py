@@ -216,12 +216,16 @@ def inverse(values: np.ndarray, a, b) -> np.ndarray:
     return np.ascontiguousarray(X)
 
 
-def forward_axes(coeffs: np.ndarray, a, b, axes) -> np.ndarray:
-    """Apply Phi along the listed axes only (used by the slab-decomposition host tests)."""
+def forward_axes(coeffs: np.ndarray, a, b, axes, points=None, kind: int = 0) -> np.ndarray:
+    """Apply the axis matrices along the listed axes only (bench's bounded CPU samples; slab host tests).
+    points / kind as in `forward_ex` (default: the uniform first-kind Phi)."""
     X = np.asarray(coeffs, dtype=np.float64)
     a, b = _params(X.shape, a, b)
     for ax in axes:
-        X = _mode_product(phi(X.shape[ax], a[ax], b[ax]), X, ax)
+        pts = None if points is None else points[ax]
+        M = phi(X.shape[ax], a[ax], b[ax]) if (pts is None and kind == 0) else axis_matrix(X.shape[ax], a[ax], b[ax],
+                                                                                            pts, kind)
+        X = _mode_product(M, X, ax)
     return np.ascontiguousarray(X)
 
 

@@ -23,7 +23,26 @@ CONFIGS = {
                         inverse=True),
     "cfg5_3d_512": dict(n=(512, 512, 512), a=(0.25, 0.25, 0.25), b=(-0.25, -0.25, -0.25),
                         eps=1e-12, inverse=False),
+    # SURVEY.md §8(f) NEXT rows (not BASELINE configs): the paper's 3D nonuniform experiment setting
+    # (a = b = 0.4 on every axis, random points) and a second-kind (Q~) uniform transform
+    "nu_3d_256": dict(n=(256, 256, 256), a=(0.4, 0.4, 0.4), b=(0.4, 0.4, 0.4), eps=1e-12, inverse=False,
+                      points="random"),
+    "q_3d_256": dict(n=(256, 256, 256), a=(0.2, -0.4, 0.35), b=(-0.2, 0.3, 0.1), eps=1e-12, inverse=False,
+                     kind=1),
 }
+
+
+def points(n: int, seed: int) -> np.ndarray:
+    """n sorted random angles, uniform in (0, pi) (nonuniform-transform locations; no method arithmetic)."""
+    rng = np.random.default_rng(seed)
+    return np.pi * np.sort(rng.uniform(0, 1, int(n))) * (1 - 2e-6) + 1e-6
+
+
+def config_points(cfg):
+    """Per-axis point arrays of a config (None = uniform Gauss-Jacobi nodes), seeds 100 + axis."""
+    if cfg.get("points") != "random":
+        return None
+    return [points(n, 100 + i) for i, n in enumerate(cfg["n"])]
 
 
 def gaussian(shape, seed: int = 0) -> np.ndarray:
