@@ -34,9 +34,10 @@ FP64_PEAK_TFLOPS = 37.0   # measured DFMA peak (profiles/fp64_peak_r01.json); de
 K0 = 27
 
 
-def algorithmic_flops_per_point(n: int, r: int, k0: int = K0) -> float:
-    """per axis pass per point r (5 log2 N + 6) + 2 k0 (conventional FFT count)."""
-    return r * (5 * np.log2(n) + 6) + 2 * k0
+def algorithmic_flops_per_point(N: int, r: int, k0: int = K0) -> float:
+    """per axis pass per point r (5 log2 N + 6) + 2 k0 (conventional FFT count; N = the
+    axis's FFT length, k0 = its dense-block width as the plan chose it)."""
+    return r * (5 * np.log2(N) + 6) + 2 * k0
 
 
 def load_peaks():
@@ -160,13 +161,13 @@ def run_reference(args, cfg, rank: int):
     print(json.dumps(line), flush=True)
 
 
-def config_block(args, cfg, ranks):
+def config_block(args, cfg, ranks, k0s=None):
     kindtxt = ("nonuniform (random points)" if cfg.get("points") else "uniform") + (
         " second-kind Q~" if cfg.get("kind", 0) == 1 else "")
     return {"workload": f"{args.config}: {'x'.join(map(str, cfg['n']))} {kindtxt} forward, (a,b)="
                         f"{list(zip(cfg['a'], cfg['b']))}, eps={cfg['eps']}",
             "model": "none (transform)", "global_batch": 1, "seq_len": int(np.prod(cfg["n"])),
-            "ranks_per_axis": ranks, "k0": K0, "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
+            "ranks_per_axis": ranks, "k0_per_axis": k0s, "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
             "l2_policy": "inputs (8 B x prod(n)) larger than the 126 MB L2; no extra flush"}
 
 
@@ -205,6 +206,8 @@ def main():
     if world == 1:
         plan = jt.Plan(shape, a, b, eps, points=si.config_points(cfg), kind=cfg.get("kind", 0))
         ranks = [plan.rank(i) for i in range(d)]
+        infos = [plan.info(i) for i in range(d)]
+        k0s = [inf["k0"] for inf in infos]
         x = torch.from_numpy(si.gaussian(shape, seed=0)).cuda()
         y = torch.empty_like(x)
         strides = []
@@ -225,6 +228,7 @@ def main():
     else:
         plan = SlabPlan(shape, a, b, eps, dist)
         ranks = plan.ranks
+        k0s = [plan.plan.info(i)["k0"] for i in range(d)]
         x = plan.local_input(torch.from_numpy(si.gaussian(shape, seed=0)))
         step = plan.make_forward_step(x)
         launches_per_step = plan.launches_per_step
@@ -272,8 +276,7 @@ def main():
         # dominant kernel: the fused forward axis pass (all d launches are this kernel; take the slowest axis)
         i_dom = int(np.argmax(per_axis_ms))
         ax_dom = strides[i_dom][0]
-        n_ax = shape[ax_dom]
-        flops = algorithmic_flops_per_point(n_ax, ranks[ax_dom]) * total_points
+        flops = algorithmic_flops_per_point(infos[ax_dom]["N"], ranks[ax_dom], k0s[ax_dom]) * total_points
         achieved = flops / (per_axis_ms[i_dom] * 1e-3) / 1e12
         traffic = None
         try:
@@ -347,7 +350,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "coefficients/s", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) fp64, numpy PCG64 seed 0",
-                "config": config_block(args, cfg, ranks), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "config": config_block(args, cfg, ranks, k0s), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -115,7 +115,7 @@ def jt_default_opts() -> jt_opts:
     return o
 
 
-def jt_plan(n, a, b, eps: float = 1e-12, seed: int = 0, k0: int = 27, rmax_init: int = 0, q: int = 3,
+def jt_plan(n, a, b, eps: float = 1e-12, seed: int = 0, k0: int = -1, rmax_init: int = 0, q: int = 3,
             sweeps: int = 2, device: int = -1, points=None, kind: int = JT_KIND_P) -> int:
     """Build a plan (C: jt_plan, or jt_plan_ex when `points` / `kind` are given).
 

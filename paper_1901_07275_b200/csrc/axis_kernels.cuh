@@ -50,14 +50,16 @@ struct AxisDev {
   const double2 *v;      // r x N        v_l[k] at v[l N + k] (zero for k < k0 and k >= n)
   const double2 *ub;     // r x MAXR x nbins   u~_l of row bstart[m] + c at ub[(l MAXR + c) nbins + m] (0-padded)
   const double *phivb;   // k0 x MAXR x nbins  (W V)[bstart[m] + c, k] at phivb[(k MAXR + c) nbins + m] (0-padded)
-  const double *phivc;   // the same in chunks of 2 degrees: (W V)[bstart[m] + c, 2 l + kk] at
-                         // phivc[((l nbins + m) MAXR + c) 2 + kk], l < ceil(k0 / 2) (0-padded)
+  const double *phivc;   // the same in chunks of VST_KPT degrees: (W V)[bstart[m] + c, KPT l + kk] at
+                         // phivc[((l nbins + m) MAXR + c) KPT + kk], l < ceil(k0 / KPT) (0-padded)
   const int *bstart;     // nbins + 1 row offsets: rows of bin m are bstart[m] .. bstart[m+1]-1
   const double2 *tw;     // per-pass twiddle tables, see TwOff (pass NS, radix RS: (RS-1) NS entries,
                          // entry (r-1) NS + j = e^{+2 pi i j r / (NS RS)})
 };
 
-constexpr int K0MAX = 32;
+constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
+constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
+                            // (4 measured slower: a bigger stage leaves room for only 2 ring stages)
 constexpr int SMEM_LIMIT = 227 * 1024;
 
 // Radix of the Stockham pass that starts at sub-transform size NS.
@@ -130,7 +132,7 @@ struct Cfg {
   // layout [m][c][kk], so the dense low-degree block is applied inside the term loop from SMEM]
   static constexpr bool STAGED = N <= 1024;
   static constexpr bool VST = N <= 512;
-  static constexpr int KPT = VST ? 2 : 0;
+  static constexpr int KPT = VST ? VST_KPT : 0;
   static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
   static constexpr int STAGE_BYTES = STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : 0;
   // twiddle tables of the passes after the first, copied to SMEM (TWS): every twiddle is one broadcast

@@ -212,8 +212,9 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   p->dev[axis].maxr = MAXR;
   std::vector<double2> ub((size_t)r * nbins * MAXR, make_double2(0.0, 0.0)), v((size_t)r * N), tw(N);
   std::vector<double> phivb((size_t)std::max(k0, 1) * nbins * MAXR, 0.0);
-  const int nchunk = std::max((k0 + 1) / 2, 1);
-  std::vector<double> phivc((size_t)nchunk * nbins * MAXR * 2, 0.0);
+  constexpr int KPT = jtk::VST_KPT;  // chunk size of the kernels' staged W V (degrees per rank term)
+  const int nchunk = std::max((k0 + KPT - 1) / KPT, 1);
+  std::vector<double> phivc((size_t)nchunk * nbins * MAXR * KPT, 0.0);
   for (int64_t m = 0; m < nbins; ++m) {
     for (int c = 0; c < h.bstart[m + 1] - h.bstart[m]; ++c) {
       const int64_t j = h.bstart[m] + c;
@@ -223,7 +224,7 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
       }
       for (int k = 0; k < k0; ++k) {
         phivb[((size_t)k * MAXR + c) * nbins + m] = h.phiv[(size_t)j * k0 + k];
-        phivc[(((size_t)(k / 2) * nbins + m) * MAXR + c) * 2 + (k % 2)] = h.phiv[(size_t)j * k0 + k];
+        phivc[(((size_t)(k / KPT) * nbins + m) * MAXR + c) * KPT + (k % KPT)] = h.phiv[(size_t)j * k0 + k];
       }
     }
   }
@@ -377,7 +378,7 @@ const char *jt_version(void) { return "jt 0.1 (sm_100a fused fp64 axis passes)";
 jt_status jt_default_opts(jt_opts *o) {
   if (!o) return fail(JT_ERR_ARG, "null opts");
   o->seed = 0;
-  o->k0 = 27;
+  o->k0 = -1;  // auto: 27 (the paper's) or 32 where that lowers the rank (R24)
   o->rmax_init = 0;
   o->q = 3;
   o->sweeps = 2;
@@ -401,7 +402,7 @@ jt_status jt_plan_ex(jt_plan_t *out, int d, const int64_t n[], const double a[],
   jt_opts o;
   jt_default_opts(&o);
   if (opts) o = *opts;
-  if (o.k0 < 0 || o.k0 > 32) return fail(JT_ERR_ARG, "k0 must be in [0, 32]");
+  if (o.k0 < -1 || o.k0 > jtk::K0MAX) return fail(JT_ERR_ARG, "k0 must be -1 (auto) or in [0, 32]");
   for (int i = 0; i < d; ++i) {
     if (n[i] < 2 || n[i] > 4096) return fail(JT_ERR_ARG, "n[i] must be in [2, 4096]");
     if (!(a[i] > -1 && a[i] < 1 && b[i] > -1 && b[i] < 1))
@@ -435,7 +436,18 @@ jt_status jt_plan_ex(jt_plan_t *out, int d, const int64_t n[], const double a[],
         continue;
       }
       std::string err;
-      jt_status s = jt::build_axis_host(p->host[i], n[i], a[i], b[i], eps, o, err, pts, kind);
+      jt_opts oa = o;
+      if (o.k0 == -1) oa.k0 = 27;
+      jt_status s = jt::build_axis_host(p->host[i], n[i], a[i], b[i], eps, oa, err, pts, kind);
+      if (s == JT_OK && o.k0 == -1 && p->host[i].N <= 512 && n[i] > 32) {
+        // auto k0 (reading R24): the kernels stage 2 degrees of W V per rank term for N <= 512, so a
+        // 32-degree block is free of extra passes; keep it if it saves a rank term
+        jt::AxisHost alt;
+        std::string err2;
+        oa.k0 = 32;
+        if (jt::build_axis_host(alt, n[i], a[i], b[i], eps, oa, err2, pts, kind) == JT_OK && alt.r < p->host[i].r)
+          p->host[i] = std::move(alt);
+      }
       if (s != JT_OK) {
         delete p;
         return fail(s, "axis " + std::to_string(i) + ": " + err);

@@ -243,3 +243,14 @@ def test_amplitude_non_oscillatory():
     M2, P = M2[50:], P[50:]  # fine grid resolving the oscillation (period 2 pi / 2000)
     # no oscillation: second differences tiny compared with those of P~^2
     assert np.max(np.abs(np.diff(M2, 2))) < 1e-3 * np.max(np.abs(np.diff(P[:, 2000] ** 2, 2)))
+
+
+def test_auto_k0():
+    """k0 = -1 (default, R24): the paper's 27, or 32 when that lowers the rank for FFT lengths
+    <= 512; explicit k0 values are kept."""
+    p = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2)
+    r27 = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2, k0=27).rank()
+    r32 = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2, k0=32).rank()
+    assert p.info()["k0"] == (32 if r32 < r27 else 27) and p.rank() == min(r27, r32)
+    assert jt.Plan(1024, 0.25, -0.3, 1e-12, device=-2).info()["k0"] == 27  # FFT length > 512
+    assert jt.Plan(512, 0.25, -0.25, 1e-12, device=-2, k0=20).info()["k0"] == 20

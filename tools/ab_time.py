@@ -15,7 +15,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(lib, configs, reps):
+def child(lib, configs, reps, k0=None):
     sys.path.insert(0, ROOT)
     import numpy as np
     import torch
@@ -35,7 +35,13 @@ def child(lib, configs, reps):
         a = (ctypes.c_double * d)(*c["a"])
         b = (ctypes.c_double * d)(*c["b"])
         h = P()
-        assert L.jt_plan(ctypes.byref(h), d, n, a, b, c["eps"], None) == 0
+        opts = None
+        if k0 is not None:  # jt_opts {seed, k0, rmax_init, q, sweeps, device}
+            class O(ctypes.Structure):
+                _fields_ = [("seed", ctypes.c_uint64), ("k0", ctypes.c_int), ("rmax_init", ctypes.c_int),
+                            ("q", ctypes.c_int), ("sweeps", ctypes.c_int), ("device", ctypes.c_int)]
+            opts = ctypes.byref(O(0, k0, 0, 3, 2, -1))
+        assert L.jt_plan(ctypes.byref(h), d, n, a, b, c["eps"], opts) == 0
         x = torch.from_numpy(si.gaussian(c["n"], 0)).cuda()
         y = torch.empty_like(x)
         s = torch.cuda.current_stream().cuda_stream
@@ -62,16 +68,20 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--k0", type=int, default=None)
     args = ap.parse_args()
     configs = args.configs.split(",")
     if args.child:
-        child(args.libs[0], configs, args.reps)
+        child(args.libs[0], configs, args.reps, args.k0)
         return
     res = {}
     for rnd in range(args.rounds):
         for lib in args.libs:
-            p = subprocess.run([sys.executable, __file__, lib, "--child", "--configs", args.configs, "--reps",
-                                str(args.reps)], capture_output=True, text=True)
+            lib_k0 = lib.split("@")
+            cmd = [sys.executable, __file__, lib_k0[0], "--child", "--configs", args.configs, "--reps", str(args.reps)]
+            if len(lib_k0) > 1:
+                cmd += ["--k0", lib_k0[1]]
+            p = subprocess.run(cmd, capture_output=True, text=True)
             line = [ln for ln in p.stdout.splitlines() if ln.startswith("RESULT ")]
             if not line:
                 print(lib, "FAILED", p.stderr[-2000:])
@@ -79,7 +89,7 @@ def main():
             r = json.loads(line[0][7:])
             for k, v in r.items():
                 res.setdefault(k, {}).setdefault(os.path.basename(lib), []).append(v)
-    names = [os.path.basename(l) for l in args.libs]
+    names = [os.path.basename(l) for l in args.libs]  # LIB.so@K0 runs the library with jt_opts.k0 = K0
     print(f"{'case':28s} " + " ".join(f"{n:>22s}" for n in names))
     for k, d in res.items():
         print(f"{k:28s} " + " ".join(f"{'/'.join(f'{v:.3f}' for v in d.get(n, [])):>22s}" for n in names))
