@@ -180,12 +180,15 @@ def main():
     ap.add_argument("--config", default="cfg5_3d_512", choices=list(si.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="run the slab-distributed path (NCCL all-to-all) even at world size 1 (path check)")
     args = ap.parse_args()
     cfg = si.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     args.warmup = max(args.warmup, 3)
+    slab = world > 1 or args.slab
 
     if args.impl == "reference":
         run_reference(args, cfg, rank)
@@ -195,7 +198,7 @@ def main():
     import paper_1901_07275_b200 as jt
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    if slab:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_1901_07275_b200.dist import SlabPlan
@@ -203,7 +206,7 @@ def main():
     d = len(shape)
     stream = torch.cuda.current_stream()
 
-    if world == 1:
+    if not slab:
         plan = jt.Plan(shape, a, b, eps, points=si.config_points(cfg), kind=cfg.get("kind", 0))
         ranks = [plan.rank(i) for i in range(d)]
         infos = [plan.info(i) for i in range(d)]
@@ -241,7 +244,7 @@ def main():
         dist.barrier()
     sampler = ClockSampler(local_rank)
     time.sleep(0.3)
-    nev = (d + 1) if world == 1 else 2
+    nev = (d + 1) if not slab else 2
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
     torch.cuda.synchronize()
     if dist is not None:
@@ -250,7 +253,7 @@ def main():
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for k in range(args.steps):
-        if world == 1:
+        if not slab:
             step(evs[k])
         else:
             step()
@@ -270,7 +273,7 @@ def main():
 
     roofline = None
     per_axis_ms = None
-    if world == 1:
+    if not slab:
         per_axis = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(d)] for k in range(args.steps)])
         per_axis_ms = per_axis.mean(axis=0)  # in launch order (axis d-1 first)
         # dominant kernel: the fused forward axis pass (all d launches are this kernel; take the slowest axis)
@@ -297,7 +300,7 @@ def main():
                                    "148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 derived"}
 
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if not slab and not args.no_e2e:
         xh = torch.from_numpy(si.gaussian(shape, seed=0)).pin_memory()
         yh = torch.empty_like(xh).pin_memory()
         xn, yn = xh.numpy(), yh.numpy()
@@ -317,7 +320,7 @@ def main():
                "ms_per_step": ms_e2e,
                "api": "jt_forward_host (pinned host buffers; chunked H2D overlapped with the axis-2/1 passes, "
                       "axis-0 pass in column blocks overlapped with the D2H)"}
-    elif world > 1 and not args.no_e2e:
+    elif slab and not args.no_e2e:
         xh = plan.local_input(torch.from_numpy(si.gaussian(shape, seed=0))).cpu().pin_memory()
         yh = torch.empty(plan.y_shape, dtype=torch.float64).pin_memory()
         xd = torch.empty_like(xh, device="cuda")

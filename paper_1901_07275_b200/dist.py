@@ -95,10 +95,7 @@ class SlabPlan:
 
     # ---- exchange ----
     def _exchange(self):
-        if self.G == 1:
-            self._recv.copy_(self._send)
-        else:
-            self.dist.all_to_all_single(self._recv, self._send, group=self.group)
+        self.dist.all_to_all_single(self._recv, self._send, group=self.group)
 
     # ---- transforms ----
     def forward(self, x, out=None):

@@ -254,3 +254,30 @@ def test_axis_pass_split_arguments_rejected():
         assert ei.value.status == jt.JT_ERR_ARG
     with pytest.raises(jt.JTError):  # chunk-major in place
         jt.jt_axis_pass(p.handle, 0, False, x, x, 1, 10, 1, 2)
+
+
+def test_slab_plan_nccl_world1():
+    """The NCCL all-to-all path of SlabPlan (world size 1: the collective is a self-copy) against the oracle:
+    exercises the same code bench.py runs under torchrun on N GPUs."""
+    import socket
+    import torch.distributed as dist
+    from paper_1901_07275_b200.dist import SlabPlan
+    if not dist.is_available() or not dist.is_nccl_available():
+        pytest.skip("no NCCL")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        shape, a, b = (48, 40, 36), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)
+        sp = SlabPlan(shape, a, b, 1e-12, dist)
+        x = si.gaussian(shape, seed=13)
+        y = sp.forward(sp.local_input(x))
+        assert relerr(y.cpu().numpy(), oracle.forward(x, a, b)) <= TOL
+        z = sp.inverse(y)
+        assert relerr(z.cpu().numpy(), x) <= TOL
+        sp.close()
+    finally:
+        dist.destroy_process_group()
