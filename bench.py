@@ -201,7 +201,7 @@ def main():
     if slab:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        from paper_1901_07275_b200.dist import SlabPlan
+        from paper_1901_07275_b200.dist import LibSlabPlan
     shape, a, b, eps = cfg["n"], cfg["a"], cfg["b"], cfg["eps"]
     d = len(shape)
     stream = torch.cuda.current_stream()
@@ -229,9 +229,9 @@ def main():
         launches_per_step = d
         local_points = int(np.prod(shape))
     else:
-        plan = SlabPlan(shape, a, b, eps, dist)
+        plan = LibSlabPlan(shape, a, b, eps, dist)
         ranks = plan.ranks
-        k0s = [plan.plan.info(i)["k0"] for i in range(d)]
+        k0s = [inf["k0"] for inf in plan.infos]
         x = plan.local_input(torch.from_numpy(si.gaussian(shape, seed=0)))
         step = plan.make_forward_step(x)
         launches_per_step = plan.launches_per_step
@@ -341,8 +341,8 @@ def main():
         ms_e2e = float(t.item())
         e2e = {"value": total_points / (ms_e2e * 1e-3), "unit": "coefficients/s",
                "h2d_bytes_per_step": int(8 * total_points), "d2h_bytes_per_step": int(8 * total_points),
-               "ms_per_step": ms_e2e, "api": "SlabPlan.forward_host per rank (pinned slabs; H2D + passes + "
-                                             "NCCL all-to-all + D2H), max over ranks"}
+               "ms_per_step": ms_e2e, "api": "jt_forward_host on the distributed plan per rank (pinned slabs; "
+                                             "H2D + passes + NCCL all-to-all + D2H), max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

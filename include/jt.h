@@ -136,6 +136,24 @@ jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, 
 jt_status jt_axis_pass(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
                        int64_t inner, int in_split, int out_split, void *cuda_stream);
 
+/* ---- slab-distributed plans ----
+ * One process per GPU.  Rank 0 calls jt_dist_unique_id and broadcasts the 128-byte id (e.g. over the
+ * torch process group); every rank then calls jt_plan_dist with the same n, a, b, eps, opts.  The library
+ * creates and owns an NCCL communicator (libnccl.so.2 is loaded on first use; JT_ERR_NCCL if absent or on
+ * any NCCL failure).  Rank g of G holds
+ *     forward input / inverse output:  the x-slab  [g n0/G, (g+1) n0/G) x n1 (x n2), C-order
+ *     forward output / inverse input:  the y-slab  n0 x [g n1/G, (g+1) n1/G) (x n2), C-order
+ * (jt_local_box).  jt_forward / jt_inverse / *_host on a distributed plan take and return these local
+ * slabs (out of place) and run: the local axis passes, ONE all-to-all (grouped ncclSend/ncclRecv on the
+ * caller's stream) of equal contiguous chunks written directly by the preceding axis pass (chunk-major
+ * layout, see jt_axis_pass), then the remaining axis pass.  d must be 2 or 3 and G must divide n0 and n1. */
+jt_status jt_dist_unique_id(void *nccl_unique_id /* 128 bytes, written */);
+jt_status jt_plan_dist(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
+                       const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks);
+/* Index box [lo, hi) of this rank's block: which = 0 the forward input (x-slab), 1 the forward output
+ * (y-slab).  Non-distributed plans return the whole array. */
+jt_status jt_local_box(jt_plan_t p, int which, int64_t lo[], int64_t hi[]);
+
 /* Free a plan (device buffers included).  jt_destroy(NULL) is JT_OK. */
 jt_status jt_destroy(jt_plan_t p);
 

@@ -31,7 +31,8 @@ _STATUS = {0: "JT_OK", 1: "JT_ERR_ARG", 2: "JT_ERR_DOMAIN", 3: "JT_ERR_NUMERIC",
            5: "JT_ERR_CUDA", 6: "JT_ERR_NCCL"}
 
 # Every symbol declared in include/jt.h and include/jt_debug.h (checked by tests/test_abi.py).
-EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_kind", "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
+EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_kind", "jt_dist_unique_id",
+            "jt_plan_dist", "jt_local_box", "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
             "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_destroy", "jt_plan_rank", "jt_plan_info",
             "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_error", "jt_version",
             "jt_debug_modified_pq"]
@@ -56,6 +57,10 @@ _lib.jt_default_opts.argtypes = [ctypes.POINTER(jt_opts)]
 _lib.jt_plan.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double, ctypes.POINTER(jt_opts)]
 _lib.jt_plan_ex.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_void_p, ctypes.c_int,
                             ctypes.c_double, ctypes.POINTER(jt_opts)]
+_lib.jt_dist_unique_id.argtypes = [ctypes.c_void_p]
+_lib.jt_plan_dist.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double, ctypes.POINTER(jt_opts),
+                              ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+_lib.jt_local_box.argtypes = [_P, ctypes.c_int, _I64, _I64]
 _lib.jt_plan_kind.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
 for _f in ("jt_forward", "jt_inverse", "jt_adjoint", "jt_forward_host", "jt_inverse_host"):
     getattr(_lib, _f).argtypes = [_P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
@@ -158,6 +163,37 @@ def jt_forward(plan: int, coeffs, values, stream=None):
 
 def jt_inverse(plan: int, values, coeffs, stream=None):
     _check(_lib.jt_inverse(plan, _ptr(values), _ptr(coeffs), _stream_handle(stream)), "jt_inverse")
+
+
+def jt_dist_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.jt_dist_unique_id(buf), "jt_dist_unique_id")
+    return buf.raw
+
+
+def jt_plan_dist(n, a, b, eps: float, uid: bytes, rank: int, nranks: int, seed: int = 0, k0: int = -1,
+                 device: int = -1) -> int:
+    """Slab-distributed plan with a library-owned NCCL communicator (C: jt_plan_dist)."""
+    n = [int(v) for v in np.atleast_1d(n)]
+    d = len(n)
+    a = np.broadcast_to(np.asarray(a, dtype=np.float64), (d,)).copy()
+    b = np.broadcast_to(np.asarray(b, dtype=np.float64), (d,)).copy()
+    o = jt_default_opts()
+    o.seed, o.k0, o.device = seed, k0, device
+    if len(uid) != 128:
+        raise ValueError("uid must be the 128-byte NCCL unique id")
+    h = _P()
+    idbuf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(_lib.jt_plan_dist(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D),
+                             b.ctypes.data_as(_D), float(eps), ctypes.byref(o), idbuf, rank, nranks), "jt_plan_dist")
+    return h.value
+
+
+def jt_local_box(plan: int, which: int, d: int):
+    lo, hi = (ctypes.c_int64 * d)(), (ctypes.c_int64 * d)()
+    _check(_lib.jt_local_box(plan, which, lo, hi), "jt_local_box")
+    return tuple(lo), tuple(hi)
 
 
 def jt_adjoint(plan: int, values, coeffs, stream=None):

@@ -3,6 +3,7 @@
 // PAPER.md:718-722): one fused kernel launch per axis, the first reading the input array, the rest in
 // place on the output array.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -52,6 +53,48 @@ struct DeviceGuard {
 
 }  // namespace
 
+// ---- NCCL, loaded on first use (dlopen of libnccl.so.2: the one torch already loaded, else the system's) ----
+namespace nccl {
+typedef struct { char internal[128]; } UniqueId;
+typedef void *Comm;
+enum { Success = 0, Float64 = 8 };
+struct Api {
+  bool ok = false;
+  std::string why;
+  int (*GetUniqueId)(UniqueId *) = nullptr;
+  int (*CommInitRank)(Comm *, int, UniqueId, int) = nullptr;
+  int (*CommDestroy)(Comm) = nullptr;
+  int (*Send)(const void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*Recv)(void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(int) = nullptr;
+};
+Api &api() {
+  static Api a = [] {
+    Api r;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      r.why = std::string("dlopen libnccl.so.2: ") + dlerror();
+      return r;
+    }
+    r.GetUniqueId = (int (*)(UniqueId *))dlsym(h, "ncclGetUniqueId");
+    r.CommInitRank = (int (*)(Comm *, int, UniqueId, int))dlsym(h, "ncclCommInitRank");
+    r.CommDestroy = (int (*)(Comm))dlsym(h, "ncclCommDestroy");
+    r.Send = (int (*)(const void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclSend");
+    r.Recv = (int (*)(void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclRecv");
+    r.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
+    r.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+    r.GetErrorString = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
+    r.ok = r.GetUniqueId && r.CommInitRank && r.CommDestroy && r.Send && r.Recv && r.GroupStart && r.GroupEnd &&
+           r.GetErrorString;
+    if (!r.ok) r.why = "libnccl.so.2 lacks a required symbol";
+    return r;
+  }();
+  return a;
+}
+}  // namespace nccl
+
 struct jt_plan_s {
   int d = 0;
   int64_t n[3] = {0, 0, 0};
@@ -64,6 +107,12 @@ struct jt_plan_s {
   double *stage_in = nullptr, *stage_out = nullptr;  // for the *_host entry points
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;      // their copy streams
   cudaEvent_t ev[2 * 16 + 2] = {};                     // and events
+  // slab-distributed plans (jt_plan_dist): this rank's x-slab (forward input) / y-slab
+  // (forward output) of the global n[0] x n[1] (x n[2]) array, the all-to-all buffers and the NCCL comm
+  bool dist = false;
+  int rank = 0, nranks = 1;
+  nccl::Comm comm = nullptr;
+  double *a2a_send = nullptr, *a2a_recv = nullptr;
 };
 
 namespace {
@@ -192,6 +241,10 @@ void free_device(jt_plan_s *p) {
   cudaFree(p->stage_in);
   cudaFree(p->stage_out);
   p->stage_in = p->stage_out = nullptr;
+  cudaFree(p->a2a_send);
+  cudaFree(p->a2a_recv);
+  p->a2a_send = p->a2a_recv = nullptr;
+  if (p->comm) nccl::api().CommDestroy(p->comm), p->comm = nullptr;
   for (auto &e : p->ev)
     if (e) cudaEventDestroy(e), e = nullptr;
   if (p->s_h2d) cudaStreamDestroy(p->s_h2d), p->s_h2d = nullptr;
@@ -281,12 +334,58 @@ jt_status check_device_plan(const jt_plan_s *p) {
 }
 
 // Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
+// One all-to-all of equal contiguous chunks (send chunk g to rank g) on stream s.
+jt_status all_to_all(const jt_plan_s *p, cudaStream_t s) {
+  nccl::Api &A = nccl::api();
+  const size_t chunk = (size_t)p->total / p->nranks;
+  int e = A.GroupStart();
+  for (int g = 0; g < p->nranks && e == nccl::Success; ++g) {
+    e = A.Send(p->a2a_send + g * chunk, chunk, nccl::Float64, g, p->comm, s);
+    if (e == nccl::Success) e = A.Recv(p->a2a_recv + g * chunk, chunk, nccl::Float64, g, p->comm, s);
+  }
+  const int e2 = A.GroupEnd();
+  if (e != nccl::Success || e2 != nccl::Success)
+    return fail(JT_ERR_NCCL, std::string("all-to-all: ") + A.GetErrorString(e != nccl::Success ? e : e2));
+  return JT_OK;
+}
+
+// Slab schedule of a distributed plan (the C twin of paper_1901_07275_b200/dist.py SlabPlan):
+//   forward: axes d-1..1 on the x-slab (axis 1 written chunk-major), all-to-all, axis 0 on the y-slab;
+//   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major.
+jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
+  const int G = p->nranks, d = p->d;
+  const long long n0 = p->n[0], n1 = p->n[1], r = d == 3 ? p->n[2] : 1;
+  jt_status st;
+  if (!inverse) {
+    if (d == 3) {
+      if ((st = launch_axis(p, 2, false, in, out, (n0 / G) * n1, 1, s)) != JT_OK) return st;
+      if ((st = launch_axis(p, 1, false, out, p->a2a_send, n0 / G, r, s, 1, G)) != JT_OK) return st;
+    } else if ((st = launch_axis(p, 1, false, in, p->a2a_send, n0 / G, 1, s, 1, G)) != JT_OK) {
+      return st;
+    }
+    if ((st = all_to_all(p, s)) != JT_OK) return st;
+    return launch_axis(p, 0, false, p->a2a_recv, out, 1, (n1 / G) * r, s);
+  }
+  if (d == 3) {
+    if ((st = launch_axis(p, 2, true, in, out, n0 * (n1 / G), 1, s)) != JT_OK) return st;
+    if ((st = launch_axis(p, 0, true, out, p->a2a_send, 1, (n1 / G) * r, s, 1, G)) != JT_OK) return st;
+  } else if ((st = launch_axis(p, 0, true, in, p->a2a_send, 1, n1 / G, s, 1, G)) != JT_OK) {
+    return st;
+  }
+  if ((st = all_to_all(p, s)) != JT_OK) return st;
+  return launch_axis(p, 1, true, p->a2a_recv, out, n0 / G, r, s, G, 1);
+}
+
 jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   jt_status st = check_device_plan(p);
   if (st != JT_OK) return st;
   if (!in || !out) return fail(JT_ERR_ARG, "null data pointer");
   if (overlaps_partially(in, out, p->total)) return fail(JT_ERR_ARG, "input and output partially overlap");
   DeviceGuard g(p->device);
+  if (p->dist) {
+    if (in == out) return fail(JT_ERR_ARG, "distributed transforms are out of place (x-slab and y-slab differ)");
+    return transform_dist(p, inverse, in, out, s);
+  }
   const double *src = in;
   for (int axis = p->d - 1; axis >= 0; --axis) {
     long long outer = 1, inner = 1;
@@ -315,6 +414,13 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
     JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
     for (auto &e : p->ev) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (p->dist) {  // slabs: copy in, transform (with the all-to-all), copy out
+    JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in, in_h, bytes, cudaMemcpyHostToDevice, s));
+    if ((st = transform(p, inverse, p->stage_in, p->stage_out, s)) != JT_OK) return st;
+    JT_CUDA_TRY(cudaMemcpyAsync(out_h, p->stage_out, bytes, cudaMemcpyDeviceToHost, s));
+    JT_CUDA_TRY(cudaStreamSynchronize(s));
+    return JT_OK;
   }
   const int d = p->d;
   const long long n0 = p->n[0];
@@ -551,6 +657,69 @@ jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, 
 jt_status jt_axis_pass(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
                        int64_t inner, int in_split, int out_split, void *stream) {
   return axis_entry(p, axis, inverse != 0, in, out, outer, inner, in_split, out_split, stream);
+}
+
+jt_status jt_dist_unique_id(void *nccl_unique_id) {
+  if (!nccl_unique_id) return fail(JT_ERR_ARG, "null id");
+  nccl::Api &A = nccl::api();
+  if (!A.ok) return fail(JT_ERR_NCCL, A.why);
+  nccl::UniqueId id;
+  const int e = A.GetUniqueId(&id);
+  if (e != nccl::Success) return fail(JT_ERR_NCCL, std::string("ncclGetUniqueId: ") + A.GetErrorString(e));
+  std::memcpy(nccl_unique_id, &id, sizeof(id));
+  return JT_OK;
+}
+
+jt_status jt_plan_dist(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
+                       const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks) {
+  if (!out) return fail(JT_ERR_ARG, "null out");
+  *out = nullptr;
+  if (d != 2 && d != 3) return fail(JT_ERR_ARG, "distributed plans need d = 2 or 3");
+  if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return fail(JT_ERR_ARG, "bad rank / nranks / id");
+  if (!n || n[0] % nranks != 0 || n[1] % nranks != 0)
+    return fail(JT_ERR_ARG, "n[0] and n[1] must be divisible by nranks");
+  if (opts && opts->device == -2) return fail(JT_ERR_ARG, "distributed plans need a device");
+  nccl::Api &A = nccl::api();
+  if (!A.ok) return fail(JT_ERR_NCCL, A.why);
+  jt_plan_t p = nullptr;
+  jt_status st = jt_plan(&p, d, n, a, b, eps, opts);
+  if (st != JT_OK) return st;
+  p->dist = true;
+  p->rank = rank;
+  p->nranks = nranks;
+  p->total /= nranks;  // local slab elements
+  DeviceGuard g(p->device);
+  nccl::UniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  const int e = A.CommInitRank(&p->comm, nranks, id, rank);
+  if (e != nccl::Success) {
+    std::string msg = std::string("ncclCommInitRank: ") + A.GetErrorString(e);
+    p->comm = nullptr;
+    jt_destroy(p);
+    return fail(JT_ERR_NCCL, msg);
+  }
+  const size_t bytes = (size_t)p->total * sizeof(double);
+  if (cudaMalloc((void **)&p->a2a_send, bytes) != cudaSuccess || cudaMalloc((void **)&p->a2a_recv, bytes) != cudaSuccess) {
+    jt_destroy(p);
+    return fail(JT_ERR_ALLOC, "all-to-all buffers");
+  }
+  *out = p;
+  return JT_OK;
+}
+
+jt_status jt_local_box(jt_plan_t p, int which, int64_t lo[], int64_t hi[]) {
+  if (!p || !lo || !hi || (which != 0 && which != 1)) return fail(JT_ERR_ARG, "bad args");
+  for (int i = 0; i < p->d; ++i) {
+    lo[i] = 0;
+    hi[i] = p->n[i];
+  }
+  if (p->dist) {
+    const int ax = which == 0 ? 0 : 1;
+    const int64_t c = p->n[ax] / p->nranks;
+    lo[ax] = p->rank * c;
+    hi[ax] = (p->rank + 1) * c;
+  }
+  return JT_OK;
 }
 
 jt_status jt_destroy(jt_plan_t p) {

@@ -172,3 +172,82 @@ class SlabPlan:
         if self.plan is not None:
             self.plan.close()
             self.plan = None
+
+
+class LibSlabPlan:
+    """The same slab-distributed transform with the schedule AND the all-to-all inside libjt.so
+    (jt_plan_dist: a library-owned NCCL communicator, grouped ncclSend/ncclRecv on the caller's stream).
+    torch.distributed is only used to broadcast the 128-byte NCCL unique id from rank 0.  This is the path
+    bench.py times; `SlabPlan` above is its host-side twin used by the gloo CPU tests."""
+
+    def __init__(self, shape, a, b, eps, dist, group=None, **plan_kw):
+        import torch
+        from . import jt_destroy, jt_dist_unique_id, jt_local_box, jt_plan_dist, jt_plan_info, jt_plan_rank
+        self.shape = tuple(int(v) for v in shape)
+        self.d = len(self.shape)
+        self.G = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if self.rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(jt_dist_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, src=0, group=group)
+        self.handle = jt_plan_dist(self.shape, a, b, eps, bytes(uid.cpu().numpy().tobytes()), self.rank, self.G,
+                                   **plan_kw)
+        self._destroy = jt_destroy
+        self.ranks = [jt_plan_rank(self.handle, i) for i in range(self.d)]
+        self.infos = [jt_plan_info(self.handle, i) for i in range(self.d)]
+        lo0, hi0 = jt_local_box(self.handle, 0, self.d)
+        lo1, hi1 = jt_local_box(self.handle, 1, self.d)
+        self.box = {0: (lo0, hi0), 1: (lo1, hi1)}
+        self.x_shape = tuple(h - l for l, h in zip(lo0, hi0))
+        self.y_shape = tuple(h - l for l, h in zip(lo1, hi1))
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.launches_per_step = self.d  # axis passes (the all-to-all is NCCL's)
+
+    def local_box(self, which: int):
+        return self.box[which]
+
+    def local_input(self, full):
+        import torch
+        lo, hi = self.box[0]
+        return torch.as_tensor(full)[lo[0]:hi[0]].contiguous().to(self.device)
+
+    def local_output(self, full):
+        import torch
+        lo, hi = self.box[1]
+        return torch.as_tensor(full)[:, lo[1]:hi[1]].contiguous().to(self.device)
+
+    def forward(self, x, out=None):
+        import torch
+        from . import jt_forward
+        out = torch.empty(self.y_shape, dtype=torch.float64, device=self.device) if out is None else out
+        jt_forward(self.handle, x, out)
+        return out
+
+    def inverse(self, y, out=None):
+        import torch
+        from . import jt_inverse
+        out = torch.empty(self.x_shape, dtype=torch.float64, device=self.device) if out is None else out
+        jt_inverse(self.handle, y, out)
+        return out
+
+    def forward_host(self, x_host, y_host, x_dev=None, y_dev=None):
+        """End-to-end forward of this rank's slab from / to (pinned) host memory (C: jt_forward_host)."""
+        from . import jt_forward_host
+        jt_forward_host(self.handle, x_host.numpy(), y_host.numpy())
+        return y_host
+
+    def make_forward_step(self, x):
+        import torch
+        out = torch.empty(self.y_shape, dtype=torch.float64, device=self.device)
+
+        def step():
+            self.forward(x, out)
+            return out
+        step.out = out
+        return step
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._destroy(self.handle)
+            self.handle = None

@@ -271,13 +271,17 @@ def test_slab_plan_nccl_world1():
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                             device_id=torch.device("cuda", torch.cuda.current_device()))
     try:
-        shape, a, b = (48, 40, 36), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)
-        sp = SlabPlan(shape, a, b, 1e-12, dist)
-        x = si.gaussian(shape, seed=13)
-        y = sp.forward(sp.local_input(x))
-        assert relerr(y.cpu().numpy(), oracle.forward(x, a, b)) <= TOL
-        z = sp.inverse(y)
-        assert relerr(z.cpu().numpy(), x) <= TOL
-        sp.close()
+        from paper_1901_07275_b200.dist import LibSlabPlan
+        for shape, a, b in [((48, 40, 36), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)),
+                            ((64, 80), (0.1, -0.25), (-0.4, 0.35))]:
+            x = si.gaussian(shape, seed=13)
+            for cls in (SlabPlan, LibSlabPlan):  # torch-collective twin and the library-owned NCCL path
+                sp = cls(shape, a, b, 1e-12, dist)
+                assert sp.local_box(0) == ((0,) * len(shape), shape)
+                y = sp.forward(sp.local_input(x))
+                assert relerr(y.cpu().numpy(), oracle.forward(x, a, b)) <= TOL, cls
+                z = sp.inverse(y)
+                assert relerr(z.cpu().numpy(), x) <= TOL, cls
+                sp.close()
     finally:
         dist.destroy_process_group()
