@@ -273,9 +273,13 @@ def main():
 
     roofline = None
     per_axis_ms = None
+    step_stats = None
     if not slab:
         per_axis = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(d)] for k in range(args.steps)])
         per_axis_ms = per_axis.mean(axis=0)  # in launch order (axis d-1 first)
+        step_ms = per_axis.sum(axis=1)       # each timed step (CUDA events on the launching stream)
+        step_stats = {"median": round(float(np.median(step_ms)), 4), "min": round(float(step_ms.min()), 4),
+                      "max": round(float(step_ms.max()), 4)}
         # dominant kernel: the fused forward axis pass (all d launches are this kernel; take the slowest axis)
         i_dom = int(np.argmax(per_axis_ms))
         ax_dom = strides[i_dom][0]
@@ -354,7 +358,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) fp64, numpy PCG64 seed 0",
                 "config": config_block(args, cfg, ranks, k0s), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+                "ms_per_step_stats": step_stats}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
