@@ -38,6 +38,7 @@
 #include <stdint.h>
 
 #include "fft_regs.cuh"
+#include "tmem.cuh"
 
 namespace jtk {
 
@@ -119,13 +120,19 @@ struct Cfg {
   // the input state lives in a thread-private SMEM area (PRIV), read once per term (8 B per point), and
   // the exchange runs one real plane at a time (SPLITX) to leave SMEM for the factor ring.
   static constexpr bool PRIV = R >= 32;
+  // PRIV state in tensor memory (TPRIV, tcgen05.ld/st): frees the SMEM crossbar of the per-term state re-reads
+#ifndef JT_TPRIV
+#define JT_TPRIV 1
+#endif
+  static constexpr bool TPRIV = PRIV && JT_TPRIV && N <= 1024;  // (N >= 2048: more register spills)
   static constexpr bool SPLITX = R >= 32;
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
   static constexpr int REGS = R >= 32 ? 255 : (MAXR > 2 ? 200 : 168);
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;
-  static constexpr int PSLOTS = PRIV ? (R > NB * MAXR ? R : NB * MAXR) : 0;  // private doubles per thread
+  static constexpr int PSTATE = PRIV ? (R > NB * MAXR ? R : NB * MAXR) : 0;  // private doubles per thread
+  static constexpr int PSLOTS = TPRIV ? 0 : PSTATE;                           // ... of them in SMEM
   // + (inverse) the per-warp partial sums of (W V)^T y (K0MAX x GW x LG)
   static constexpr int VRED = INV ? K0MAX * GW * LG : 0;
   static constexpr int GROUP_BYTES = ((SLOTS * XB + K0MAX * LG * 8 + PSLOTS * GT * 8 + VRED * 8) + 127) / 128 * 128;
@@ -164,6 +171,10 @@ struct Cfg {
   static_assert(GT % 32 == 0, "group must be whole warps");
   static_assert(RSL >= 2, "last pass radix");
   static_assert(smem_bytes() <= SMEM_LIMIT, "shared memory");
+  // TMEM: 512 columns; the NT/32 warps share the 4 lane quadrants, each warp a column slice of TCOLS
+  static constexpr int NWARP = NT / 32;
+  static constexpr int TCOLS = NWARP >= 4 ? 512 / (NWARP / 4) : 512;
+  static_assert(!TPRIV || (NWARP % 4 == 0 && (PSTATE + 15) / 16 * 32 <= TCOLS), "TMEM state slice");
 };
 
 __device__ __forceinline__ const double2 *tw_smem_base(int off) {
@@ -424,6 +435,7 @@ __device__ __forceinline__ constexpr int fwd_reg_of_bin(int q) {
 template <class C>
 struct Ctx {
   int grp, gt, line, vt;
+  uint32_t tbase = 0, taddr = 0;  // TMEM allocation base / this thread's state slice (C::TPRIV)
   void *buf;     // group exchange buffer
   double *alow;  // group: k0 x LG low-degree coefficients (forward) / reduced a_V (inverse)
   double *priv;  // group: thread-private slots [slot][gt] (C::PRIV)
@@ -496,7 +508,26 @@ struct Ctx {
       const int j0 = __ldg(&bstart[m]);
       binfo()[i] = (j0 << 4) | (__ldg(&bstart[m + 1]) - j0);
     }
+    __shared__ uint32_t tslot;
+    if constexpr (C::TPRIV) {
+      if (threadIdx.x < 32) tmem_alloc(&tslot, 512);  // one CTA per SM: all 512 columns
+      tmem_fence_before_sync();
+    }
     __syncthreads();
+    if constexpr (C::TPRIV) {
+      tmem_fence_after_sync();
+      tbase = tslot;
+      const int w = threadIdx.x / 32;
+      taddr = tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)((w / 4) * C::TCOLS);
+    }
+  }
+  // end of the kernel: every warp's TMEM traffic done, then warp 0 frees the allocation
+  __device__ __forceinline__ void finish() {
+    if constexpr (C::TPRIV) {
+      tmem_fence_before_sync();
+      __syncthreads();
+      if (threadIdx.x < 32) tmem_dealloc(tbase, 512);
+    }
   }
   __device__ __forceinline__ const double2 *vfac(long long seq, int l) const {
     if constexpr (C::STAGED) return ring.v(seq);
@@ -514,21 +545,47 @@ struct Ctx {
   }
 };
 
-// S doubles of per-thread state: registers, or (C::PRIV) the thread's private SMEM slots.  Indices are
-// compile-time constants after unrolling.
+// S doubles of per-thread state: registers, or (C::PRIV) private slots in tensor memory (C::TPRIV: the
+// thread's TMEM lane, 16 doubles per tcgen05.ld pair) or in SMEM.  Written once per batch (store), read once
+// per rank term in chunks of CH = 16 (chunk: includes the wait for the TMEM load).
 template <class C, int S>
 struct State {
+  static constexpr int CH = 16, NCH = (S + CH - 1) / CH;
   double reg[C::PRIV ? 1 : S];
   double *sm;
   int gt;
-  __device__ __forceinline__ State(double *p, int t) : sm(p), gt(t) {}
-  __device__ __forceinline__ double get(int i) const {
-    if constexpr (C::PRIV) return sm[i * C::GT + gt];
-    else return reg[i];
+  uint32_t taddr;
+  __device__ __forceinline__ State(double *p, int t, uint32_t ta) : sm(p), gt(t), taddr(ta) {}
+  __device__ __forceinline__ void store(const double (&v)[S]) {
+    if constexpr (!C::PRIV) {
+#pragma unroll
+      for (int i = 0; i < S; ++i) reg[i] = v[i];
+    } else if constexpr (C::TPRIV) {
+#pragma unroll
+      for (int c = 0; c < 2 * NCH; ++c) {  // 8 doubles (16 columns) per store, zero padded
+        double t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = (c * 8 + i < S) ? v[c * 8 + i] : 0.0;
+        tmem_st_d8(taddr + 16 * c, t);
+      }
+      tmem_wait_st();
+    } else {
+#pragma unroll
+      for (int i = 0; i < S; ++i) sm[i * C::GT + gt] = v[i];
+    }
   }
-  __device__ __forceinline__ void set(int i, double v) {
-    if constexpr (C::PRIV) sm[i * C::GT + gt] = v;
-    else reg[i] = v;
+  __device__ __forceinline__ void chunk(int c, double (&o)[CH]) const {
+    if constexpr (!C::PRIV) {
+#pragma unroll
+      for (int i = 0; i < CH; ++i) o[i] = (c * CH + i < S) ? reg[c * CH + i] : 0.0;
+    } else if constexpr (C::TPRIV) {
+      tmem_ld_d8(taddr + 32 * c, &o[0]);
+      tmem_ld_d8(taddr + 32 * c + 16, &o[8]);
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int i = 0; i < CH; ++i) o[i] = (c * CH + i < S) ? sm[(c * CH + i) * C::GT + gt] : 0.0;
+    }
   }
 };
 
@@ -594,7 +651,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 
     // coefficients at the first-pass input positions k = vt + r TPL; degrees < k0 also to alow
     // (all loads issued before any shared-memory store, so that their latencies overlap)
-    State<C, R> a(cx.priv, cx.gt);
+    State<C, R> a(cx.priv, cx.gt, cx.taddr);
     {
       double av[R];
 #pragma unroll
@@ -602,10 +659,10 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
         const int k = vt + r * TPL;
         av[r] = (live && k < n) ? __ldg(&in[ia.at(k)]) : 0.0;
       }
+      a.store(av);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int k = vt + r * TPL;
-        a.set(r, av[r]);
         if (r * TPL < K0MAX && k < K0MAX) cx.alow[k * LG + line] = k < k0 ? av[r] : 0.0;  // zero pad: W V pairs
       }
     }
@@ -650,11 +707,18 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       }
       double xr[R], xi[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {  // A1
-        const double2 vv = vl[vt + r * TPL];
-        const double ar = a.get(r);
-        xr[r] = vv.x * ar;
-        xi[r] = vv.y * ar;
+      for (int ch = 0; ch < State<C, R>::NCH; ++ch) {  // A1
+        double ac[State<C, R>::CH];
+        a.chunk(ch, ac);
+#pragma unroll
+        for (int i = 0; i < State<C, R>::CH; ++i) {
+          const int r = ch * State<C, R>::CH + i;
+          if (r < R) {
+            const double2 vv = vl[vt + r * TPL];
+            xr[r] = vv.x * ac[i];
+            xi[r] = vv.y * ac[i];
+          }
+        }
       }
       fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30));  // A2 (opaque offset: no hoisting of twiddles)
 #pragma unroll
@@ -685,6 +749,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
     }
     group_sync<C>();  // alow / PRIV reuse by the next batch
   }
+  cx.finish();
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -715,7 +780,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
     const LineAddr<SPLIT> ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
     const LineAddr<SPLIT> oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
 
-    State<C, NB * MAXR> yb(cx.priv, cx.gt);  // yb(q MAXR + c): row c of input bin q
+    State<C, NB * MAXR> yb(cx.priv, cx.gt, cx.taddr);  // element q MAXR + c: row c of input bin q
     {
       // a_V = (W V)^T y: thread partial sums over its rows (held in registers here: nothing else is
       // live yet), reduced over the TPL threads of the line (shuffles within the warp, then SMEM across
@@ -729,8 +794,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
 #pragma unroll
         for (int c = 0; c < MAXR; ++c) yr[q * MAXR + c] = (live && own && c < cnt) ? __ldg(&in[ia.at(j0 + c)]) : 0.0;
       }
-#pragma unroll
-      for (int i = 0; i < NB * MAXR; ++i) yb.set(i, yr[i]);
+      yb.store(yr);
       double *red = static_cast<double *>(cx.buf);  // k0 x GW x LG partials (exchange buffer is free)
       for (int k = kin; k < k0; ++k) {
         const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
@@ -781,11 +845,20 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       for (int r = 0; r < R; ++r) {
         xr[r] = 0.0;
         xi[r] = 0.0;
-        if (r <= R / 2) {  // bin sums (positions > N/2 hold no rows)
+      }
+      // bin sums over the rows of the input bins q <= R/2 (positions > N/2 hold no rows), state read in chunks
+      using YS = State<C, NB * MAXR>;
 #pragma unroll
-          for (int c = 0; c < MAXR; ++c) {
+      for (int ch = 0; ch < YS::NCH; ++ch) {
+        double yc[YS::CH];
+        yb.chunk(ch, yc);
+#pragma unroll
+        for (int i = 0; i < YS::CH; ++i) {
+          const int idx = ch * YS::CH + i;
+          if (idx < NB * MAXR) {
+            const int r = idx / MAXR, c = idx % MAXR;
             const double2 uu = ul[c * NBINS + m[r]];
-            const double yv = yb.get(r * MAXR + c);
+            const double yv = yc[i];
             xr[r] = fma(uu.x, yv, xr[r]);
             xi[r] = fma(uu.y, yv, xi[r]);
             if constexpr (C::VST) {
@@ -845,6 +918,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
     }
     group_sync<C>();
   }
+  cx.finish();
 }
 
 }  // namespace jtk
