@@ -125,7 +125,13 @@ struct Cfg {
 #define JT_TPRIV 1
 #endif
   static constexpr bool TPRIV = PRIV && JT_TPRIV && N <= 1024;  // (N >= 2048: more register spills)
-  static constexpr bool SPLITX = R >= 32;
+#ifndef JT_SPLITX_TPRIV
+#define JT_SPLITX_TPRIV 0
+#endif
+  // exchange one real plane at a time (3 group barriers per exchange) only while SMEM is short: with the state
+  // in TMEM the full complex exchange (1 barrier) fits
+  static constexpr bool SPLITX = R >= 32 && (!TPRIV || JT_SPLITX_TPRIV);
+
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
   static constexpr int REGS = R >= 32 ? 255 : (MAXR > 2 ? 200 : 168);
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
