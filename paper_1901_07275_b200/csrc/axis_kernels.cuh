@@ -124,7 +124,10 @@ struct Cfg {
 #ifndef JT_TPRIV
 #define JT_TPRIV 1
 #endif
-  static constexpr bool TPRIV = PRIV && JT_TPRIV && N <= 1024;  // (N >= 2048: more register spills)
+#ifndef JT_TPRIV_NMAX
+#define JT_TPRIV_NMAX 4096
+#endif
+  static constexpr bool TPRIV = PRIV && JT_TPRIV && N <= JT_TPRIV_NMAX;
 #ifndef JT_SPLITX_TPRIV
 #define JT_SPLITX_TPRIV 0
 #endif
