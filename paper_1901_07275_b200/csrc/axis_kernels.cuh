@@ -119,7 +119,13 @@ struct Cfg {
   // (the forward's bin rows y: 2 NB MAXR, or the inverse's acc: 2R).  For R >= 32 that exceeds 255, so
   // the input state lives in a thread-private SMEM area (PRIV), read once per term (8 B per point), and
   // the exchange runs one real plane at a time (SPLITX) to leave SMEM for the factor ring.
-  static constexpr bool PRIV = R >= 32;
+#ifndef JT_PRIV16
+#define JT_PRIV16 1
+#endif
+#ifndef JT_REGS16
+#define JT_REGS16 168
+#endif
+  static constexpr bool PRIV = R >= 32 || (JT_PRIV16 && N >= 64);
   // PRIV state in tensor memory (TPRIV, tcgen05.ld/st): frees the SMEM crossbar of the per-term state re-reads
 #ifndef JT_TPRIV
 #define JT_TPRIV 1
@@ -136,7 +142,7 @@ struct Cfg {
   static constexpr bool SPLITX = R >= 32 && (!TPRIV || JT_SPLITX_TPRIV);
 
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
-  static constexpr int REGS = R >= 32 ? 255 : (MAXR > 2 ? 200 : 168);
+  static constexpr int REGS = R >= 32 ? 255 : (PRIV ? JT_REGS16 : (MAXR > 2 ? 200 : 168));
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;
@@ -163,7 +169,7 @@ struct Cfg {
   }
   static constexpr int gpc_fit(int g, int nstage) {
     return (g > 1 && (((g * GT + 127) / 128) * 128 * REGS > 65536 || g * GROUP_BYTES + hdr_bytes(nstage) > SMEM_LIMIT ||
-                      g * GW > 15 || g * GT > 1024))
+                      g > 15 || g * GT > 1024))  // named barriers 1..15 (one per group)
                ? gpc_fit(g - 1, nstage)
                : g;
   }
