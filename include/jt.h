@@ -116,6 +116,15 @@ jt_status jt_inverse(jt_plan_t p, const double *values, double *coeffs, void *cu
 jt_status jt_forward_host(jt_plan_t p, const double *coeffs_host, double *values_host, void *cuda_stream);
 jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs_host, void *cuda_stream);
 
+/* Asynchronous variants: enqueue the same pipelined work and return; results are in host memory after
+ * jt_host_wait(p).  Consecutive calls alternate between two plan-owned staging slots, so one call's input copy
+ * (host->device engine) overlaps the previous call's output copy (device->host engine) and compute: a stream
+ * of transforms runs at the rate of the slower PCIe direction.  The host buffers must stay valid and unmodified
+ * until jt_host_wait.  Calls on one plan must come from one host thread. */
+jt_status jt_forward_host_async(jt_plan_t p, const double *coeffs_host, double *values_host, void *cuda_stream);
+jt_status jt_inverse_host_async(jt_plan_t p, const double *values_host, double *coeffs_host, void *cuda_stream);
+jt_status jt_host_wait(jt_plan_t p);
+
 /* One axis pass (the building block of the slab-distributed schedule):
  * applies axis `axis`'s 1D forward (inverse) transform along the middle index of an
  * (outer, n[axis], inner) C-order device array.  in == out allowed (in place). */

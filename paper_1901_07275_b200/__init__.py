@@ -32,7 +32,8 @@ _STATUS = {0: "JT_OK", 1: "JT_ERR_ARG", 2: "JT_ERR_DOMAIN", 3: "JT_ERR_NUMERIC",
 
 # Every symbol declared in include/jt.h and include/jt_debug.h (checked by tests/test_abi.py).
 EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_kind", "jt_dist_unique_id",
-            "jt_plan_dist", "jt_local_box", "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
+            "jt_plan_dist", "jt_local_box", "jt_forward_host_async", "jt_inverse_host_async", "jt_host_wait",
+            "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
             "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_destroy", "jt_plan_rank", "jt_plan_info",
             "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_error", "jt_version",
             "jt_debug_modified_pq"]
@@ -62,7 +63,9 @@ _lib.jt_plan_dist.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ct
                               ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 _lib.jt_local_box.argtypes = [_P, ctypes.c_int, _I64, _I64]
 _lib.jt_plan_kind.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
-for _f in ("jt_forward", "jt_inverse", "jt_adjoint", "jt_forward_host", "jt_inverse_host"):
+_lib.jt_host_wait.argtypes = [_P]
+for _f in ("jt_forward", "jt_inverse", "jt_adjoint", "jt_forward_host", "jt_inverse_host", "jt_forward_host_async",
+           "jt_inverse_host_async"):
     getattr(_lib, _f).argtypes = [_P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 for _f in ("jt_forward_axis", "jt_inverse_axis"):
     getattr(_lib, _f).argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
@@ -217,6 +220,20 @@ def jt_inverse_host(plan: int, values_host: np.ndarray, coeffs_host: np.ndarray,
            "jt_inverse_host")
 
 
+def jt_forward_host_async(plan: int, coeffs_host: np.ndarray, values_host: np.ndarray, stream=None):
+    _check(_lib.jt_forward_host_async(plan, _ptr(coeffs_host), _ptr(values_host), _stream_handle(stream)),
+           "jt_forward_host_async")
+
+
+def jt_inverse_host_async(plan: int, values_host: np.ndarray, coeffs_host: np.ndarray, stream=None):
+    _check(_lib.jt_inverse_host_async(plan, _ptr(values_host), _ptr(coeffs_host), _stream_handle(stream)),
+           "jt_inverse_host_async")
+
+
+def jt_host_wait(plan: int):
+    _check(_lib.jt_host_wait(plan), "jt_host_wait")
+
+
 def jt_forward_axis(plan: int, axis: int, x_in, x_out, outer: int, inner: int, stream=None):
     _check(_lib.jt_forward_axis(plan, axis, _ptr(x_in), _ptr(x_out), outer, inner, _stream_handle(stream)),
            "jt_forward_axis")
@@ -335,6 +352,14 @@ class Plan:
         out = np.empty(self.shape) if out is None else out
         jt_inverse_host(self.handle, values, out, stream)
         return out
+
+    def forward_host_async(self, coeffs: np.ndarray, out: np.ndarray, stream=None):
+        """Enqueue a host-buffer forward transform (results valid after wait_host()); see include/jt.h."""
+        jt_forward_host_async(self.handle, coeffs, out, stream)
+        return out
+
+    def wait_host(self):
+        jt_host_wait(self.handle)
 
     def rank(self, axis: int = 0) -> int:
         return jt_plan_rank(self.handle, axis)

@@ -104,9 +104,13 @@ struct jt_plan_s {
   jt::AxisHost host[3];
   AxisDevBuf dev[3];
   int64_t total = 0;
-  double *stage_in = nullptr, *stage_out = nullptr;  // for the *_host entry points
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;      // their copy streams
-  cudaEvent_t ev[2 * 16 + 2] = {};                     // and events
+  // *_host entry points: two staging slots (consecutive calls alternate, so one call's input copy overlaps the
+  // previous call's output copy), their copy streams and events
+  double *stage_in[2] = {nullptr, nullptr}, *stage_out[2] = {nullptr, nullptr};
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev[2 * 16 + 2] = {};
+  cudaEvent_t ev_free[2] = {nullptr, nullptr};  // slot's last output copy done
+  unsigned host_calls = 0;
   // slab-distributed plans (jt_plan_dist): this rank's x-slab (forward input) / y-slab
   // (forward output) of the global n[0] x n[1] (x n[2]) array, the all-to-all buffers and the NCCL comm
   bool dist = false;
@@ -238,9 +242,12 @@ void free_device(jt_plan_s *p) {
     cudaFree(p->dev[i].bstart);
     p->dev[i] = AxisDevBuf();
   }
-  cudaFree(p->stage_in);
-  cudaFree(p->stage_out);
-  p->stage_in = p->stage_out = nullptr;
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(p->stage_in[k]);
+    cudaFree(p->stage_out[k]);
+    p->stage_in[k] = p->stage_out[k] = nullptr;
+    if (p->ev_free[k]) cudaEventDestroy(p->ev_free[k]), p->ev_free[k] = nullptr;
+  }
   cudaFree(p->a2a_send);
   cudaFree(p->a2a_recv);
   p->a2a_send = p->a2a_recv = nullptr;
@@ -402,75 +409,84 @@ jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *
 // chunk); the axis-0 pass then runs in KC column blocks, each copied back (a pitched 2D copy) on a second
 // copy stream while the next block computes.  Every line runs the same kernel code as in jt_forward /
 // jt_inverse, so the results are bitwise identical to the device path.
-jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double *out_h, cudaStream_t s) {
+jt_status host_wait(jt_plan_s *p) {
+  if (!p->s_d2h) return JT_OK;
+  DeviceGuard g(p->device);
+  JT_CUDA_TRY(cudaStreamSynchronize(p->s_h2d));
+  JT_CUDA_TRY(cudaStreamSynchronize(p->s_d2h));
+  return JT_OK;
+}
+
+jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double *out_h, cudaStream_t s,
+                         bool wait) {
   jt_status st = check_device_plan(p);
   if (st != JT_OK) return st;
   if (!in_h || !out_h) return fail(JT_ERR_ARG, "null host pointer");
   DeviceGuard g(p->device);
   const size_t bytes = (size_t)p->total * sizeof(double);
-  if (!p->stage_in) {
-    if (cudaMalloc((void **)&p->stage_in, bytes) != cudaSuccess) return fail(JT_ERR_ALLOC, "staging cudaMalloc");
-    if (cudaMalloc((void **)&p->stage_out, bytes) != cudaSuccess) return fail(JT_ERR_ALLOC, "staging cudaMalloc");
+  if (!p->s_h2d) {
     JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
     JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
     for (auto &e : p->ev) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : p->ev_free) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  if (p->dist) {  // slabs: copy in, transform (with the all-to-all), copy out
-    JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in, in_h, bytes, cudaMemcpyHostToDevice, s));
-    if ((st = transform(p, inverse, p->stage_in, p->stage_out, s)) != JT_OK) return st;
-    JT_CUDA_TRY(cudaMemcpyAsync(out_h, p->stage_out, bytes, cudaMemcpyDeviceToHost, s));
-    JT_CUDA_TRY(cudaStreamSynchronize(s));
-    return JT_OK;
+  const int slot = (int)(p->host_calls++ & 1u);
+  if (!p->stage_in[slot]) {
+    if (cudaMalloc((void **)&p->stage_in[slot], bytes) != cudaSuccess ||
+        cudaMalloc((void **)&p->stage_out[slot], bytes) != cudaSuccess)
+      return fail(JT_ERR_ALLOC, "staging cudaMalloc");
+    JT_CUDA_TRY(cudaEventRecord(p->ev_free[slot], p->s_d2h));
   }
-  const int d = p->d;
-  const long long n0 = p->n[0];
-  const long long row = p->total / n0;  // elements per axis-0 index (the axis-0 pass's line count)
-  const int KC = (d == 1) ? 1 : (int)std::min<long long>(8, n0);
-  cudaEvent_t *ev_in = p->ev, *ev_out = p->ev + 16, ev_start = p->ev[32], ev_done = p->ev[33];
-  // the copy streams start after all prior work on s (the caller's ordering)
+  double *sin = p->stage_in[slot], *sout = p->stage_out[slot];
+  cudaEvent_t *ev_in = p->ev, *ev_out = p->ev + 16, ev_start = p->ev[32];
+  // ordering: the caller's prior work on s first; the slot's previous use (its output copy) finished
   JT_CUDA_TRY(cudaEventRecord(ev_start, s));
-  JT_CUDA_TRY(cudaStreamWaitEvent(p->s_h2d, ev_start, 0));
+  JT_CUDA_TRY(cudaStreamWaitEvent(p->s_h2d, p->ev_free[slot], 0));
+  JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_free[slot], 0));
   JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_start, 0));
-  if (d == 1) {
-    JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in, in_h, bytes, cudaMemcpyHostToDevice, s));
-    if ((st = transform(p, inverse, p->stage_in, p->stage_out, s)) != JT_OK) return st;
-    JT_CUDA_TRY(cudaMemcpyAsync(out_h, p->stage_out, bytes, cudaMemcpyDeviceToHost, s));
-    JT_CUDA_TRY(cudaStreamSynchronize(s));
-    return JT_OK;
-  }
-  // phase 1: row chunks of axis 0
-  for (int c = 0; c < KC; ++c) {
-    const long long r0 = n0 * c / KC, r1 = n0 * (c + 1) / KC;
-    const size_t off = (size_t)(r0 * row), cnt = (size_t)((r1 - r0) * row);
-    JT_CUDA_TRY(cudaMemcpyAsync(p->stage_in + off, in_h + off, cnt * sizeof(double), cudaMemcpyHostToDevice,
-                                p->s_h2d));
-    JT_CUDA_TRY(cudaEventRecord(ev_in[c], p->s_h2d));
-    JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[c], 0));
-    const double *src = p->stage_in + off;
-    for (int axis = d - 1; axis >= 1; --axis) {
-      long long outer = r1 - r0, inner = 1;
-      for (int i = 1; i < axis; ++i) outer *= p->n[i];
-      for (int i = axis + 1; i < d; ++i) inner *= p->n[i];
-      if ((st = launch_axis(p, axis, inverse, src, p->stage_out + off, outer, inner, s)) != JT_OK) return st;
-      src = p->stage_out + off;
+  const int d = p->d;
+  if (p->dist || d == 1) {  // slabs (with the all-to-all) / one line: copy in, transform, copy out
+    JT_CUDA_TRY(cudaMemcpyAsync(sin, in_h, bytes, cudaMemcpyHostToDevice, p->s_h2d));
+    JT_CUDA_TRY(cudaEventRecord(ev_in[0], p->s_h2d));
+    JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[0], 0));
+    if ((st = transform(p, inverse, sin, sout, s)) != JT_OK) return st;
+    JT_CUDA_TRY(cudaEventRecord(ev_out[0], s));
+    JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[0], 0));
+    JT_CUDA_TRY(cudaMemcpyAsync(out_h, sout, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
+  } else {
+    const long long n0 = p->n[0];
+    const long long row = p->total / n0;  // elements per axis-0 index (the axis-0 pass's line count)
+    const int KC = (int)std::min<long long>(8, n0);
+    // phase 1: row chunks of axis 0 arrive on the copy stream; axes d-1..1 run on each arrived chunk
+    for (int c = 0; c < KC; ++c) {
+      const long long r0 = n0 * c / KC, r1 = n0 * (c + 1) / KC;
+      const size_t off = (size_t)(r0 * row), cnt = (size_t)((r1 - r0) * row);
+      JT_CUDA_TRY(cudaMemcpyAsync(sin + off, in_h + off, cnt * sizeof(double), cudaMemcpyHostToDevice, p->s_h2d));
+      JT_CUDA_TRY(cudaEventRecord(ev_in[c], p->s_h2d));
+      JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[c], 0));
+      const double *src = sin + off;
+      for (int axis = d - 1; axis >= 1; --axis) {
+        long long outer = r1 - r0, inner = 1;
+        for (int i = 1; i < axis; ++i) outer *= p->n[i];
+        for (int i = axis + 1; i < d; ++i) inner *= p->n[i];
+        if ((st = launch_axis(p, axis, inverse, src, sout + off, outer, inner, s)) != JT_OK) return st;
+        src = sout + off;
+      }
+    }
+    // phase 2: axis-0 pass in column blocks, each copied back (pitched) while the next computes
+    for (int c = 0; c < KC; ++c) {
+      const long long c0 = row * c / KC, c1 = row * (c + 1) / KC;
+      if (c1 == c0) continue;
+      if ((st = launch_axis(p, 0, inverse, sout + c0, sout + c0, 1, row, s, 1, 1, c1 - c0)) != JT_OK) return st;
+      JT_CUDA_TRY(cudaEventRecord(ev_out[c], s));
+      JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[c], 0));
+      JT_CUDA_TRY(cudaMemcpy2DAsync(out_h + c0, (size_t)row * sizeof(double), sout + c0, (size_t)row * sizeof(double),
+                                    (size_t)(c1 - c0) * sizeof(double), (size_t)n0, cudaMemcpyDeviceToHost,
+                                    p->s_d2h));
     }
   }
-  // phase 2: axis-0 pass in column blocks, each copied back while the next computes
-  for (int c = 0; c < KC; ++c) {
-    const long long c0 = row * c / KC, c1 = row * (c + 1) / KC;
-    if (c1 == c0) continue;
-    if ((st = launch_axis(p, 0, inverse, p->stage_out + c0, p->stage_out + c0, 1, row, s, 1, 1, c1 - c0)) != JT_OK)
-      return st;
-    JT_CUDA_TRY(cudaEventRecord(ev_out[c], s));
-    JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[c], 0));
-    JT_CUDA_TRY(cudaMemcpy2DAsync(out_h + c0, (size_t)row * sizeof(double), p->stage_out + c0,
-                                  (size_t)row * sizeof(double), (size_t)(c1 - c0) * sizeof(double), (size_t)n0,
-                                  cudaMemcpyDeviceToHost, p->s_d2h));
-  }
-  JT_CUDA_TRY(cudaEventRecord(ev_done, p->s_d2h));
-  JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
-  JT_CUDA_TRY(cudaStreamSynchronize(s));
-  return JT_OK;
+  JT_CUDA_TRY(cudaEventRecord(p->ev_free[slot], p->s_d2h));
+  return wait ? host_wait(p) : JT_OK;
 }
 
 }  // namespace
@@ -619,13 +635,28 @@ jt_status jt_plan_kind(jt_plan_t p, int axis, int *uniform, int *kind) {
 }
 
 jt_status jt_forward_host(jt_plan_t p, const double *coeffs_host, double *values_host, void *stream) {
-  return transform_host(p, false, coeffs_host, values_host, (cudaStream_t)stream);
+  return transform_host(p, false, coeffs_host, values_host, (cudaStream_t)stream, true);
+}
+
+jt_status jt_forward_host_async(jt_plan_t p, const double *coeffs_host, double *values_host, void *stream) {
+  return transform_host(p, false, coeffs_host, values_host, (cudaStream_t)stream, false);
+}
+
+jt_status jt_inverse_host_async(jt_plan_t p, const double *values_host, double *coeffs_host, void *stream) {
+  jt_status st = check_orthogonal(p);
+  if (st != JT_OK) return st;
+  return transform_host(p, true, values_host, coeffs_host, (cudaStream_t)stream, false);
+}
+
+jt_status jt_host_wait(jt_plan_t p) {
+  if (!p) return fail(JT_ERR_ARG, "null plan");
+  return host_wait(p);
 }
 
 jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs_host, void *stream) {
   jt_status st = check_orthogonal(p);
   if (st != JT_OK) return st;
-  return transform_host(p, true, values_host, coeffs_host, (cudaStream_t)stream);
+  return transform_host(p, true, values_host, coeffs_host, (cudaStream_t)stream, true);
 }
 
 static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *in, double *out, int64_t outer,
