@@ -101,6 +101,26 @@ struct TwTotal<N, R, N> {
   static constexpr int value = 0;
 };
 
+// Twiddles a thread applies per FFT (complex values): passes after the first, B butterflies of RS - 1 each.
+template <int N, int R, int P = Pass<N, R, 1>::RS>
+struct TwPerThread {
+  static constexpr int value = Pass<N, R, P>::B * (Pass<N, R, P>::RS - 1) + TwPerThread<N, R, P * Pass<N, R, P>::RS>::value;
+};
+template <int N, int R>
+struct TwPerThread<N, R, N> {
+  static constexpr int value = 0;
+};
+// ... of the passes before the one at sub-size NS
+template <int N, int R, int NS, int P = Pass<N, R, 1>::RS>
+struct TwPrefix {
+  static constexpr int value =
+      (P >= NS) ? 0 : Pass<N, R, P>::B * (Pass<N, R, P>::RS - 1) + TwPrefix<N, R, NS, P * Pass<N, R, P>::RS>::value;
+};
+template <int N, int R, int NS>
+struct TwPrefix<N, R, NS, N> {
+  static constexpr int value = 0;
+};
+
 template <int N_, int R_, int MAXR_, bool INV_>
 struct Cfg {
   static constexpr int N = N_, R = R_, MAXR = MAXR_;
@@ -161,7 +181,14 @@ struct Cfg {
   // twiddle tables of the passes after the first, copied to SMEM (TWS): every twiddle is one broadcast
   // LDS.128 instead of a chain of complex multiplies
   static constexpr bool TWS = N <= 1024;
-  static constexpr int TW_BYTES = TWS ? (TwTotal<N, R>::value * 16 + 127) / 128 * 128 : 0;
+  // ... and with the state in TMEM, each thread's own twiddles (constant for the kernel) in its TMEM slice (TWT)
+#ifndef JT_TWT
+#define JT_TWT 1
+#endif
+  static constexpr int TWPT = TwPerThread<N, R>::value;  // complex twiddles per thread
+  // (MAXR 4: slice too small; the R = 32 inverse measured 2 % slower with it)
+  static constexpr bool TWT = TWS && TPRIV && JT_TWT && TWPT > 0 && MAXR == 2 && (!INV || R == 16);
+  static constexpr int TW_BYTES = (TWS && !TWT) ? (TwTotal<N, R>::value * 16 + 127) / 128 * 128 : 0;
   // per-CTA table of the row range of every (thread position vt, bin slot q): (j0 << 4) | count
   static constexpr int BINFO_BYTES = STAGED ? (TPL * NB * 4 + 127) / 128 * 128 : 0;
   static constexpr int hdr_bytes(int nstage) {
@@ -189,7 +216,12 @@ struct Cfg {
   // TMEM: 512 columns; the NT/32 warps share the 4 lane quadrants, each warp a column slice of TCOLS
   static constexpr int NWARP = NT / 32;
   static constexpr int TCOLS = NWARP >= 4 ? 512 / (NWARP / 4) : 512;
-  static_assert(!TPRIV || (NWARP % 4 == 0 && (PSTATE + 15) / 16 * 32 <= TCOLS), "TMEM state slice");
+  static constexpr int TW_COL0 = (PSTATE + 15) / 16 * 32;          // twiddles after the state chunks
+  static constexpr int TW_COLS = TWT ? (4 * TWPT + 31) / 32 * 32 : 0;
+  static constexpr bool TMEM_OK = !TPRIV || (NWARP % 4 == 0 && TW_COL0 + TW_COLS <= TCOLS);
+#ifndef JT_NO_TMEM_ASSERT
+  static_assert(TMEM_OK, "TMEM state slice");
+#endif
 };
 
 __device__ __forceinline__ const double2 *tw_smem_base(int off) {
@@ -345,15 +377,38 @@ __device__ __forceinline__ void pass_load(double (&xr)[C::R], double (&xi)[C::R]
 // Twiddle and radix-RS butterflies of the pass at sub-size NS (inputs already in registers).
 template <class C, int NS>
 __device__ __forceinline__ void pass_compute(double (&xr)[C::R], double (&xi)[C::R], int vt,
-                                             const double2 *__restrict__ tw) {
+                                             const double2 *__restrict__ tw, uint32_t ttw) {
   using P = Pass<C::N, C::R, NS>;
   constexpr int RS = P::RS;
 #pragma unroll
   for (int i = 0; i < P::B; ++i) {
     const int v = vt + i * C::TPL;
-    // Twiddles w^r, w = e^{2 pi i (v mod NS) / (NS RS)}: exact table values at the anchors r = 1 (mod 8),
-    // the rest by the chain w^r = w^{r-1} w (<= 7 roundings from an anchor).  A load costs the L1 data
-    // pipe 4 cycles per warp (tools/l1_probe.cu) while a complex multiply costs the FP64 pipe 2.
+    if constexpr (C::TWT) {
+      // this thread's twiddles w^r, r = 1..RS-1, from its TMEM slice, 8 complex per tcgen05.ld pair
+      constexpr int NCHK = (RS - 1 + 7) / 8;
+      const uint32_t t0 = ttw + 4 * (TwPrefix<C::N, C::R, NS>::value + i * (RS - 1));
+#pragma unroll
+      for (int ch = 0; ch < NCHK; ++ch) {
+        double w[16];
+        tmem_ld_d8(t0 + 32 * ch, &w[0]);
+        tmem_ld_d8(t0 + 32 * ch + 16, &w[8]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = 1 + 8 * ch + j;
+          if (r < RS) {
+            const double pr = w[2 * j], pim = w[2 * j + 1];
+            const double tr = xr[i * RS + r] * pr - xi[i * RS + r] * pim;
+            xi[i * RS + r] = fma(xr[i * RS + r], pim, xi[i * RS + r] * pr);
+            xr[i * RS + r] = tr;
+          }
+        }
+      }
+      dft<RS>(&xr[i * RS], &xi[i * RS]);
+      continue;
+    }
+    // Twiddles w^r, w = e^{2 pi i (v mod NS) / (NS RS)}: every one from the SMEM table (TWS), or exact table
+    // values at the anchors r = 1 (mod 8) and the chain w^r = w^{r-1} w in between (from global / L1).
     double pr = 1.0, pim = 0.0;
     double2 w1;
     const double2 *twp;
@@ -386,6 +441,27 @@ __device__ __forceinline__ void pass_compute(double (&xr)[C::R], double (&xi)[C:
   }
 }
 
+// Fill this thread's TMEM twiddle slice (C::TWT): for each pass after the first, for each of its butterflies i,
+// w^r (r = 1..RS-1) with w = e^{2 pi i (v mod NS) / (NS RS)}, v = vt + i TPL, copied from the global tables.
+template <class C, int NS>
+__device__ __forceinline__ void tw_fill(double *buf, int vt, const double2 *__restrict__ tw) {
+  if constexpr (NS < C::N) {
+    using P = Pass<C::N, C::R, NS>;
+#pragma unroll
+    for (int i = 0; i < P::B; ++i) {
+      const int v = vt + i * C::TPL;
+#pragma unroll
+      for (int r = 1; r < P::RS; ++r) {
+        const double2 w = __ldg(&tw[TwOff<C::N, C::R, NS>::value + (r - 1) * NS + (v % NS)]);
+        const int k = TwPrefix<C::N, C::R, NS>::value + i * (P::RS - 1) + (r - 1);
+        buf[2 * k] = w.x;
+        buf[2 * k + 1] = w.y;
+      }
+    }
+    tw_fill<C, NS * P::RS>(buf, vt, tw);
+  }
+}
+
 // Exchange the outputs of the pass that started at NSS (in registers) into the inputs of the pass at
 // NS = NSS RS(NSS).  On entry every thread of the group has finished reading the buffer.
 template <class C, int NSS>
@@ -408,13 +484,13 @@ __device__ __forceinline__ void do_exchange(double (&xr)[C::R], double (&xi)[C::
 
 template <class C, int NS>
 __device__ __forceinline__ void run_passes(double (&xr)[C::R], double (&xi)[C::R], void *buf, int vt, int line,
-                                           const double2 *__restrict__ tw) {
+                                           const double2 *__restrict__ tw, uint32_t ttw) {
   if constexpr (NS < C::N) {
-    pass_compute<C, NS>(xr, xi, vt, tw);
+    pass_compute<C, NS>(xr, xi, vt, tw, ttw);
     if constexpr (!Pass<C::N, C::R, NS>::LAST) {
       group_sync<C>();
       do_exchange<C, NS>(xr, xi, buf, vt, line);
-      run_passes<C, NS * Pass<C::N, C::R, NS>::RS>(xr, xi, buf, vt, line, tw);
+      run_passes<C, NS * Pass<C::N, C::R, NS>::RS>(xr, xi, buf, vt, line, tw, ttw);
     }
   }
 }
@@ -423,13 +499,13 @@ __device__ __forceinline__ void run_passes(double (&xr)[C::R], double (&xi)[C::R
 // outputs (positions out_pos) in registers on exit.  The caller syncs the group before the next call.
 template <class C>
 __device__ __forceinline__ void fft(double (&xr)[C::R], double (&xi)[C::R], void *buf, int vt, int line,
-                                    const double2 *__restrict__ tw) {
+                                    const double2 *__restrict__ tw, uint32_t ttw) {
   using P0 = Pass<C::N, C::R, 1>;
 #pragma unroll
   for (int i = 0; i < P0::B; ++i) dft<P0::RS>(&xr[i * P0::RS], &xi[i * P0::RS]);
   if constexpr (!P0::LAST) {
     do_exchange<C, 1>(xr, xi, buf, vt, line);
-    run_passes<C, P0::RS>(xr, xi, buf, vt, line, tw);
+    run_passes<C, P0::RS>(xr, xi, buf, vt, line, tw, ttw);
   }
 }
 
@@ -503,7 +579,7 @@ struct Ctx {
   // row-range table of the bins binof(vt, q) filled.
   template <class BinOf>
   __device__ __forceinline__ void start(const int *__restrict__ bstart, const double2 *__restrict__ tw, BinOf binof) {
-    if constexpr (C::TWS) {
+    if constexpr (C::TWS && !C::TWT) {
       extern __shared__ __align__(128) char smem_raw[];
       double2 *t = reinterpret_cast<double2 *>(smem_raw + C::TW_OFF);
       for (int i = threadIdx.x; i < TwTotal<C::N, C::R>::value; i += C::NT) t[i] = __ldg(&tw[i]);
@@ -534,6 +610,16 @@ struct Ctx {
       tbase = tslot;
       const int w = threadIdx.x / 32;
       taddr = tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)((w / 4) * C::TCOLS);
+    }
+    if constexpr (C::TWT) {  // the thread's twiddles, once for the whole kernel
+      constexpr int NV = (2 * C::TWPT + 7) / 8 * 8;
+      double t[NV];
+#pragma unroll
+      for (int i = 2 * C::TWPT; i < NV; ++i) t[i] = 0.0;
+      tw_fill<C, Pass<C::N, C::R, 1>::RS>(t, vt, tw);
+#pragma unroll
+      for (int c = 0; c < NV / 8; ++c) tmem_st_d8(taddr + C::TW_COL0 + 16 * c, &t[8 * c]);
+      tmem_wait_st();
     }
   }
   // end of the kernel: every warp's TMEM traffic done, then warp 0 frees the allocation
@@ -735,7 +821,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
           }
         }
       }
-      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30));  // A2 (opaque offset: no hoisting of twiddles)
+      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.taddr + C::TW_COL0);  // A2
 #pragma unroll
       for (int q = 0; q < NB; ++q) {  // A3
         const int e = fwd_reg_of_bin<C>(q);
@@ -901,7 +987,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
           }
         }
       }
-      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30));
+      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.taddr + C::TW_COL0);
 #pragma unroll
       for (int e = 0; e < R; ++e) {  // a[k] += Re(v_l[k] B[k])
         const double2 vv = vl[out_pos<C>(vt, e)];
