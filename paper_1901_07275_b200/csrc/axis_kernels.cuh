@@ -166,7 +166,7 @@ struct Cfg {
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;
-  static constexpr int PSTATE = PRIV ? (R > NB * MAXR ? R : NB * MAXR) : 0;  // private doubles per thread
+  static constexpr int PSTATE = PRIV ? (INV ? NB * MAXR : R) : 0;  // private doubles per thread (inverse: bin rows)
   static constexpr int PSLOTS = TPRIV ? 0 : PSTATE;                           // ... of them in SMEM
   // + (inverse) the per-warp partial sums of (W V)^T y (K0MAX x GW x LG)
   static constexpr int VRED = INV ? K0MAX * GW * LG : 0;
