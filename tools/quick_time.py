@@ -6,10 +6,10 @@ import paper_1901_07275_b200 as jt
 import seeded_inputs as si
 res = {}
 for name, c in si.CONFIGS.items():
-    t0 = time.time(); p = jt.Plan(c["n"], c["a"], c["b"], c["eps"]); tp = time.time() - t0
+    t0 = time.time(); p = jt.Plan(c["n"], c["a"], c["b"], c["eps"], points=si.config_points(c), kind=c.get("kind", 0)); tp = time.time() - t0
     x = torch.from_numpy(si.gaussian(c["n"], 0)).cuda(); y = torch.empty_like(x)
     for fn in ("fwd", "inv"):
-        f = jt.jt_forward if fn == "fwd" else jt.jt_inverse
+        f = jt.jt_forward if fn == "fwd" else jt.jt_adjoint
         for _ in range(3): f(p.handle, x, y)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
