@@ -112,7 +112,8 @@ jt_status jt_inverse(jt_plan_t p, const double *values, double *coeffs, void *cu
  * transforms, copies device->host, then synchronises `cuda_stream`.  Uses plan-owned device staging
  * buffers and two plan-owned copy streams: the input arrives in row chunks of axis 0 while the passes of
  * axes d-1..1 run on the chunks already copied; the axis-0 pass runs in column blocks, each copied back
- * while the next one computes.  Results are bitwise identical to jt_forward / jt_inverse. */
+ * while the next one computes.  Results equal jt_forward / jt_inverse up to rounding (the device path may
+ * split the rank terms of a few-line launch over several CTAs and sum them in another order). */
 jt_status jt_forward_host(jt_plan_t p, const double *coeffs_host, double *values_host, void *cuda_stream);
 jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs_host, void *cuda_stream);
 

@@ -58,6 +58,14 @@ struct AxisDev {
                          // entry (r-1) NS + j = e^{+2 pi i j r / (NS RS)})
 };
 
+// Term split (few lines: latency-bound launches).  S > 1: CTA b handles batch b / S and only the rank terms
+// [s r / S, (s + 1) r / S) of slice s = b % S (the W V block in the slices of its degrees), writing its
+// partial line results to part[(s nlines + L) n + j]; ts_reduce sums the S partials in slice order.
+struct TermSplit {
+  int S;
+  double *part;
+};
+
 constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
 constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
                             // (4 measured slower: a bigger stage leaves room for only 2 ring stages)
@@ -279,6 +287,7 @@ struct Ring {
   const double2 *gv, *gu;
   const double *gph;
   int r, k0;
+  int l0 = 0, rs = 1;  // term range of this CTA: l0 .. l0 + rs - 1
   __device__ __forceinline__ double2 *v(long long seq) const {
     return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES);
   }
@@ -290,7 +299,7 @@ struct Ring {
   }
   __device__ __forceinline__ void issue(long long seq) const {  // producer: one thread
     const int s = (int)(seq % C::NSTAGE);
-    const int l = (int)(seq % r);
+    const int l = l0 + (int)(seq % rs);
     const bool kc = C::VST && l * C::KPT < k0;  // chunk l of W V exists (zero-padded to KPT degrees)
     const uint32_t ph_bytes = kc ? C::PH_BYTES : 0;
     mbar_arrive_expect_tx(&full[s], C::V_BYTES + C::U_BYTES + ph_bytes);
@@ -523,7 +532,7 @@ __device__ __forceinline__ constexpr int fwd_reg_of_bin(int q) {
 }
 
 // Per-CTA shared-memory carve-up and per-thread group geometry.
-template <class C>
+template <class C, bool TSPLIT = false>
 struct Ctx {
   int grp, gt, line, vt;
   uint32_t tbase = 0, taddr = 0;  // TMEM allocation base / this thread's state slice (C::TPRIV)
@@ -532,9 +541,10 @@ struct Ctx {
   double *priv;  // group: thread-private slots [slot][gt] (C::PRIV)
   double *vred;  // group: K0MAX x GW x LG per-warp partials of (W V)^T y (inverse)
   Ring<C> ring;
-  long long nbatch;
+  long long nbatch, bt0, btstep;
+  int slice = 0, S = 1, l0 = 0, l1 = 0;
   const double2 *gv, *gu;
-  __device__ __forceinline__ Ctx(char *smem, const AxisDev &ax, long long nlines) {
+  __device__ __forceinline__ Ctx(char *smem, const AxisDev &ax, long long nlines, const TermSplit &ts) {
     grp = threadIdx.x / C::GT;
     gt = threadIdx.x % C::GT;
     line = gt % C::LG;
@@ -556,8 +566,25 @@ struct Ctx {
     priv = alow + K0MAX * C::LG;
     vred = priv + C::PSLOTS * C::GT;
     nbatch = (nlines + C::GPC * C::LG - 1) / (C::GPC * C::LG);
-    const long long mine = blockIdx.x < nbatch ? (nbatch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    ring.total = mine * ax.r;
+    S = TSPLIT ? ts.S : 1;
+    long long mine;
+    if (TSPLIT) {  // one (batch, term slice) per CTA
+      slice = blockIdx.x % S;
+      bt0 = blockIdx.x / S;
+      btstep = nbatch;
+      l0 = (int)((long long)slice * ax.r / S);
+      l1 = (int)((long long)(slice + 1) * ax.r / S);
+      mine = bt0 < nbatch ? 1 : 0;
+    } else {
+      bt0 = blockIdx.x;
+      btstep = gridDim.x;
+      l0 = 0;
+      l1 = ax.r;
+      mine = blockIdx.x < nbatch ? (nbatch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    }
+    ring.l0 = l0;
+    ring.rs = l1 - l0 > 0 ? l1 - l0 : 1;
+    ring.total = mine * (l1 - l0);
   }
   // CTA table: TPL x NB packed row ranges (j0 << 4) | count of the bins binof(vt, q) (staged configs;
   // the others read bstart from global: their register budget has no room for the extra live state)
@@ -706,6 +733,7 @@ struct Layout {
   int in_cs, out_cs;  // chunk length of the input / output along the axis (== n: plain C-order)
 };
 
+
 // SPLIT is a template flag (a separate kernel instantiation) so that the plain layout costs no registers.
 template <bool SPLIT>
 struct LineAddr {
@@ -727,12 +755,12 @@ struct LineAddr {
 // ------------------------------------------------------------------------------------------------
 // Forward axis pass (K4).
 // ------------------------------------------------------------------------------------------------
-template <class C, bool SPLIT>
+template <class C, bool SPLIT, bool TSPLIT = false>
 __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, Layout lay) {
+                                                             long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
-  Ctx<C> cx(smem_raw, ax, nlines);
+  Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
   cx.start(ax.bstart, ax.tw, [](int vt_, int q) { return q < R / 2 ? out_pos<C>(vt_, fwd_reg_of_bin<C>(q)) : C::N / 2; });
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
@@ -744,7 +772,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   for (int q = 0; q < NB; ++q) m[q] = q < R / 2 ? out_pos<C>(vt, fwd_reg_of_bin<C>(q)) : C::N / 2;
 
   long long seq = 0;
-  for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
+  for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
     const LineAddr<SPLIT> ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
@@ -775,7 +803,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int c = 0; c < MAXR; ++c) y[q][c] = 0.0;
     group_sync<C>();
-    for (int k = kin; k < k0; ++k) {
+    for (int k = kin; k < ((!TSPLIT || cx.slice == 0) ? k0 : kin); ++k) {
       const double ak = cx.alow[k * LG + line];
       const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
 #pragma unroll
@@ -787,7 +815,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       }
     }
 
-    for (int l = 0; l < ax.r; ++l, ++seq) {
+    for (int l = cx.l0; l < cx.l1; ++l, ++seq) {
       cx.acquire(seq);
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
@@ -844,7 +872,10 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
           cx.rows_of(ax.bstart, q, m[q], j0, cnt);
 #pragma unroll
           for (int c = 0; c < MAXR; ++c)
-            if (c < cnt) out[oa.at(j0 + c)] = y[q][c];
+            if (c < cnt) {
+              if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + j0 + c] = y[q][c];
+              else out[oa.at(j0 + c)] = y[q][c];
+            }
         }
       }
     }
@@ -856,12 +887,12 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 // ------------------------------------------------------------------------------------------------
 // Inverse axis pass (K5).
 // ------------------------------------------------------------------------------------------------
-template <class C, bool SPLIT>
+template <class C, bool SPLIT, bool TSPLIT = false>
 __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, Layout lay) {
+                                                             long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
-  Ctx<C> cx(smem_raw, ax, nlines);
+  Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
   cx.start(ax.bstart, ax.tw, [](int vt_, int q) { return q < R / 2 ? vt_ + q * TPL : C::N / 2; });
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
@@ -875,7 +906,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   for (int q = 0; q < NB; ++q) m[q] = q < R / 2 ? vt + q * TPL : C::N / 2;
 
   long long seq = 0;
-  for (long long bt = blockIdx.x; bt < cx.nbatch; bt += gridDim.x) {
+  for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
     const LineAddr<SPLIT> ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
@@ -897,7 +928,11 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       yb.store(yr);
       double *red = static_cast<double *>(cx.buf);  // k0 x GW x LG partials (exchange buffer is free)
-      for (int k = kin; k < k0; ++k) {
+      if (TSPLIT) {  // degrees outside this slice's terms contribute 0 (their slices add them)
+        for (int i = cx.gt; i < k0 * LG; i += C::GT) cx.alow[i] = 0.0;
+        for (int i = cx.gt; i < kin * C::GW * LG; i += C::GT) cx.vred[i] = 0.0;
+      }
+      for (int k = kin; k < ((!TSPLIT || cx.slice == 0) ? k0 : kin); ++k) {
         const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
         double p = 0.0;
 #pragma unroll
@@ -917,7 +952,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       if constexpr (C::GW > 1) {
         group_sync<C>();
-        for (int i = cx.gt + kin * LG; i < k0 * LG; i += C::GT) {
+        for (int i = cx.gt + kin * LG; i < ((!TSPLIT || cx.slice == 0) ? k0 : kin) * LG; i += C::GT) {
           const int k = i / LG, ln = i % LG;
           double s = 0.0;
 #pragma unroll
@@ -932,7 +967,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
 #pragma unroll
     for (int e = 0; e < R; ++e) acc[e] = 0.0;
 
-    for (int l = 0; l < ax.r; ++l, ++seq) {
+    for (int l = cx.l0; l < cx.l1; ++l, ++seq) {
       cx.acquire(seq);
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
@@ -1014,7 +1049,10 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         const int k = out_pos<C>(vt, e);
         double val = acc[e];
         if (k < k0) val += cx.alow[k * LG + line];
-        if (k < n) out[oa.at(k)] = val;
+        if (k < n) {
+          if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + k] = val;
+          else out[oa.at(k)] = val;
+        }
       }
     }
     group_sync<C>();
@@ -1022,4 +1060,20 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   cx.finish();
 }
 
+}  // namespace jtk
+
+namespace jtk {
+// Sum of the S term-slice partials of a term-split launch (slice order: deterministic), written in the plain
+// (outer, n, inner) layout.  Element (o, j, i), i fastest.
+__global__ void ts_reduce(const double *__restrict__ part, double *__restrict__ out, int S, long long nlines, int n,
+                          long long inner) {
+  const long long total = nlines * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e % inner, oj = e / inner, j = oj % n, o = oj / n;
+    const long long L = o * inner + i;
+    double sum = 0.0;
+    for (int s = 0; s < S; ++s) sum += part[((long long)s * nlines + L) * n + j];
+    out[e] = sum;
+  }
+}
 }  // namespace jtk

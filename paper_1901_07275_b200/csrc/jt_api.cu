@@ -113,6 +113,9 @@ struct jt_plan_s {
   unsigned host_calls = 0;
   // slab-distributed plans (jt_plan_dist): this rank's x-slab (forward input) / y-slab
   // (forward output) of the global n[0] x n[1] (x n[2]) array, the all-to-all buffers and the NCCL comm
+  // term-split workspace (few-line launches, jtk::TermSplit)
+  mutable double *ts_work = nullptr;
+  mutable size_t ts_elems = 0;
   bool dist = false;
   int rank = 0, nranks = 1;
   nccl::Comm comm = nullptr;
@@ -155,8 +158,8 @@ int radix_of(int64_t N, int maxr) {
 
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
 template <class C>
-jt_status launch_cfg(const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                     const jtk::Layout &lay, cudaStream_t s) {
+jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
+                     const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
   const size_t smem = C::smem_bytes();
   const long long lines_per_batch = (long long)C::GPC * C::LG;
   const long long batches = (nlines + lines_per_batch - 1) / lines_per_batch;
@@ -164,55 +167,83 @@ jt_status launch_cfg(const jtk::AxisDev &ax, const double *in, double *out, long
   int dev = 0, sms = 148;
   JT_CUDA_TRY(cudaGetDevice(&dev));
   JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned grid = (unsigned)std::min<long long>(batches, sms);
   const bool split = lay.in_cs != ax.n || lay.out_cs != ax.n;
+  // few lines (fewer batches than half the SMs): split the rank terms over S CTAs per batch and sum the
+  // partials (jtk::TermSplit, jtk::ts_reduce), so a latency-bound launch uses more of the GPU
+  jtk::TermSplit ts{1, nullptr};
+  if (allow_ts && !split && nlines == lay.outer * lay.inner && ax.r >= 2 && batches * 2 <= sms) {
+    const int S = (int)std::min<long long>(ax.r, sms / batches);
+    const size_t need = (size_t)S * nlines * ax.n;
+    if (S > 1) {
+      if (p->ts_elems < need) {
+        cudaFree(p->ts_work);
+        p->ts_work = nullptr;
+        p->ts_elems = 0;
+        if (cudaMalloc((void **)&p->ts_work, need * sizeof(double)) != cudaSuccess)
+          return fail(JT_ERR_ALLOC, "term-split workspace");
+        p->ts_elems = need;
+      }
+      ts = jtk::TermSplit{S, p->ts_work};
+    }
+  }
+  const unsigned grid = ts.S > 1 ? (unsigned)(batches * ts.S) : (unsigned)std::min<long long>(batches, sms);
   if constexpr (C::INV) {
-    auto kern = split ? jtk::inv_axis_kernel<C, true> : jtk::inv_axis_kernel<C, false>;
+    auto kern = ts.S > 1 ? jtk::inv_axis_kernel<C, false, true>
+                         : (split ? jtk::inv_axis_kernel<C, true> : jtk::inv_axis_kernel<C, false>);
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay);
+    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
   } else {
-    auto kern = split ? jtk::fwd_axis_kernel<C, true> : jtk::fwd_axis_kernel<C, false>;
+    auto kern = ts.S > 1 ? jtk::fwd_axis_kernel<C, false, true>
+                         : (split ? jtk::fwd_axis_kernel<C, true> : jtk::fwd_axis_kernel<C, false>);
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay);
+    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
   }
   JT_CUDA_TRY(cudaGetLastError());
+  if (ts.S > 1) {
+    const long long total = nlines * ax.n;
+    const int thr = 256;
+    const unsigned g = (unsigned)std::min<long long>((total + thr - 1) / thr, 4LL * sms);
+    jtk::ts_reduce<<<g, thr, 0, s>>>(ts.part, out, ts.S, nlines, ax.n, lay.inner);
+    JT_CUDA_TRY(cudaGetLastError());
+  }
   return JT_OK;
 }
 
 template <int N, int MAXR>
-jt_status launch_nm(bool inverse, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                    const jtk::Layout &lay, cudaStream_t s) {
-  if (inverse) return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, true>>(ax, in, out, nlines, lay, s);
-  return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, false>>(ax, in, out, nlines, lay, s);
+jt_status launch_nm(const jt_plan_s *p, bool inverse, const jtk::AxisDev &ax, const double *in, double *out,
+                    long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
+  if (inverse)
+    return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, true>>(p, ax, in, out, nlines, lay, s, allow_ts);
+  return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, false>>(p, ax, in, out, nlines, lay, s, allow_ts);
 }
 
 template <int N>
-jt_status launch_n(bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                   const jtk::Layout &lay, cudaStream_t s) {
-  if (maxr <= 2) return launch_nm<N, 2>(inverse, ax, in, out, nlines, lay, s);
-  return launch_nm<N, 4>(inverse, ax, in, out, nlines, lay, s);
+jt_status launch_n(const jt_plan_s *p, bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out,
+                   long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
+  if (maxr <= 2) return launch_nm<N, 2>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
+  return launch_nm<N, 4>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
 }
 
 // One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
 // layout of the slab all-to-all for the input / output.
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
                       long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
-                      long long nlines_only = -1) {
+                      long long nlines_only = -1, bool allow_ts = true) {
   jtk::AxisDev ax = axis_dev(p, axis);
   const int maxr = p->dev[axis].maxr;
   // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
   const long long nlines = nlines_only >= 0 ? nlines_only : outer * inner;
   const jtk::Layout lay{outer, inner, (int)(p->n[axis] / in_split), (int)(p->n[axis] / out_split)};
   switch (ax.N) {
-    case 16: return launch_n<16>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 32: return launch_n<32>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 64: return launch_n<64>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 128: return launch_n<128>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 256: return launch_n<256>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 512: return launch_n<512>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 1024: return launch_n<1024>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 2048: return launch_n<2048>(inverse, maxr, ax, in, out, nlines, lay, s);
-    case 4096: return launch_n<4096>(inverse, maxr, ax, in, out, nlines, lay, s);
+    case 16: return launch_n<16>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 32: return launch_n<32>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 64: return launch_n<64>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 128: return launch_n<128>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 256: return launch_n<256>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 512: return launch_n<512>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 1024: return launch_n<1024>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 2048: return launch_n<2048>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 4096: return launch_n<4096>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
     default: return fail(JT_ERR_ARG, "unsupported FFT length");
   }
 }
@@ -248,6 +279,9 @@ void free_device(jt_plan_s *p) {
     p->stage_in[k] = p->stage_out[k] = nullptr;
     if (p->ev_free[k]) cudaEventDestroy(p->ev_free[k]), p->ev_free[k] = nullptr;
   }
+  cudaFree(p->ts_work);
+  p->ts_work = nullptr;
+  p->ts_elems = 0;
   cudaFree(p->a2a_send);
   cudaFree(p->a2a_recv);
   p->a2a_send = p->a2a_recv = nullptr;
@@ -408,7 +442,7 @@ jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *
 // on a copy stream while the axis passes d-1 .. 1 run on each arrived chunk (their lines lie inside the
 // chunk); the axis-0 pass then runs in KC column blocks, each copied back (a pitched 2D copy) on a second
 // copy stream while the next block computes.  Every line runs the same kernel code as in jt_forward /
-// jt_inverse, so the results are bitwise identical to the device path.
+// jt_inverse, so the results equal the device path's up to rounding (term-split launches sum in another order).
 jt_status host_wait(jt_plan_s *p) {
   if (!p->s_d2h) return JT_OK;
   DeviceGuard g(p->device);

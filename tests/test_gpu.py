@@ -168,8 +168,10 @@ def test_host_entry_points_match_device():
     shape, a, b = (64, 64, 64), (0.1, 0.2, 0.3), (-0.1, -0.2, -0.3)
     p = jt.Plan(shape, a, b, 1e-12)
     x = si.gaussian(shape, seed=2)
-    np.testing.assert_array_equal(p.forward_host(x), gpu_forward(p, x))
-    np.testing.assert_array_equal(p.inverse_host(x), gpu_forward(p, x, inverse=True))
+    # identical up to rounding: a few-line launch may split its rank terms over CTAs (term split) where the
+    # host path's chunks do not, summing the same terms in another order
+    assert relerr(p.forward_host(x), gpu_forward(p, x)) <= 1e-14
+    assert relerr(p.inverse_host(x), gpu_forward(p, x, inverse=True)) <= 1e-14
 
 
 def test_axis_entry_points_compose():
@@ -289,7 +291,7 @@ def test_slab_plan_nccl_world1():
 
 def test_host_async_stream_matches_device():
     """jt_forward_host_async / jt_inverse_host_async: several calls in flight over the two staging slots, each
-    result bitwise equal to the device-pointer path (include/jt.h)."""
+    result equal to the device-pointer path up to rounding (include/jt.h)."""
     shape, a, b = (64, 48, 40), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)
     p = jt.Plan(shape, a, b, 1e-12)
     xs = [si.gaussian(shape, seed=30 + k) for k in range(5)]
@@ -298,13 +300,13 @@ def test_host_async_stream_matches_device():
         jt.jt_forward_host_async(p.handle, xs[k], ys[k])
     jt.jt_host_wait(p.handle)
     for k in range(5):
-        np.testing.assert_array_equal(ys[k], gpu_forward(p, xs[k]))
+        assert relerr(ys[k], gpu_forward(p, xs[k])) <= 1e-14
     zs = [np.empty(shape) for _ in range(3)]
     for k in range(3):
         jt.jt_inverse_host_async(p.handle, ys[k], zs[k])
     jt.jt_host_wait(p.handle)
     for k in range(3):
-        np.testing.assert_array_equal(zs[k], gpu_forward(p, ys[k], inverse=True))
+        assert relerr(zs[k], gpu_forward(p, ys[k], inverse=True)) <= 1e-14
         assert relerr(zs[k], xs[k]) <= TOL
 
 
