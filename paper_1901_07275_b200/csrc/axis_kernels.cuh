@@ -153,6 +153,9 @@ struct Cfg {
 #ifndef JT_REGS16
 #define JT_REGS16 168
 #endif
+#ifndef JT_REGS16F
+#define JT_REGS16F 128
+#endif
   static constexpr bool PRIV = R >= 32 || (JT_PRIV16 && N >= 64);
   // PRIV state in tensor memory (TPRIV, tcgen05.ld/st): frees the SMEM crossbar of the per-term state re-reads
 #ifndef JT_TPRIV
@@ -170,7 +173,7 @@ struct Cfg {
   static constexpr bool SPLITX = R >= 32 && (!TPRIV || JT_SPLITX_TPRIV);
 
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
-  static constexpr int REGS = R >= 32 ? 255 : (PRIV ? JT_REGS16 : (MAXR > 2 ? 200 : 168));
+  static constexpr int REGS = R >= 32 ? 255 : (PRIV ? (INV ? JT_REGS16 : JT_REGS16F) : (MAXR > 2 ? 200 : 168));
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;

@@ -148,12 +148,15 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
 #ifndef JT_R512
 #define JT_R512 32
 #endif
+#ifndef JT_R4096
+#define JT_R4096 32
+#endif
 template <int N, int MAXR>
 constexpr int radix_for() {
-  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : 32))));
+  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32)))));
 }
 int radix_of(int64_t N, int maxr) {
-  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : 32))));
+  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32)))));
 }
 
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
