@@ -198,7 +198,10 @@ struct Cfg {
 #endif
   static constexpr int TWPT = TwPerThread<N, R>::value;  // complex twiddles per thread
   // (MAXR 4: slice too small; the R = 32 inverse measured 2 % slower with it)
-  static constexpr bool TWT = TWS && TPRIV && JT_TWT && TWPT > 0 && MAXR == 2 && (!INV || R == 16);
+#ifndef JT_TWT_INV32
+#define JT_TWT_INV32 0
+#endif
+  static constexpr bool TWT = TWS && TPRIV && JT_TWT && TWPT > 0 && MAXR == 2 && (!INV || R == 16 || JT_TWT_INV32);
   static constexpr int TW_BYTES = (TWS && !TWT) ? (TwTotal<N, R>::value * 16 + 127) / 128 * 128 : 0;
   // per-CTA table of the row range of every (thread position vt, bin slot q): (j0 << 4) | count
   static constexpr int BINFO_BYTES = STAGED ? (TPL * NB * 4 + 127) / 128 * 128 : 0;
