@@ -229,10 +229,16 @@ struct Cfg {
   static_assert(smem_bytes() <= SMEM_LIMIT, "shared memory");
   // TMEM: 512 columns; the NT/32 warps share the 4 lane quadrants, each warp a column slice of TCOLS
   static constexpr int NWARP = NT / 32;
-  static constexpr int TCOLS = NWARP >= 4 ? 512 / (NWARP / 4) : 512;
+  static constexpr int TCOLS = NWARP >= 4 ? 512 / (NWARP / 4) : 512;  // column slice per warp (upper bound)
   static constexpr int TW_COL0 = (PSTATE + 15) / 16 * 32;          // twiddles after the state chunks
   static constexpr int TW_COLS = TWT ? (4 * TWPT + 31) / 32 * 32 : 0;
+  static constexpr int pow2_ge(int v, int p = 32) { return p >= v ? p : pow2_ge(v, 2 * p); }
+  // allocate only what the slices use (a power of two >= 32), so CTAs that co-reside on an SM can all allocate
+  static constexpr int TALLOC = pow2_ge((TW_COL0 + TW_COLS) * ((NWARP + 3) / 4) > 512 ? 512
+                                                                                    : (TW_COL0 + TW_COLS) * ((NWARP + 3) / 4));
+  static constexpr int TSTRIDE = TALLOC / ((NWARP + 3) / 4) / 16 * 16;
   static constexpr bool TMEM_OK = !TPRIV || (NWARP % 4 == 0 && TW_COL0 + TW_COLS <= TCOLS);
+  static_assert(!TPRIV || TW_COL0 + TW_COLS <= TSTRIDE, "TMEM slice stride");
 #ifndef JT_NO_TMEM_ASSERT
   static_assert(TMEM_OK, "TMEM state slice");
 #endif
@@ -634,7 +640,7 @@ struct Ctx {
     }
     __shared__ uint32_t tslot;
     if constexpr (C::TPRIV) {
-      if (threadIdx.x < 32) tmem_alloc(&tslot, 512);  // one CTA per SM: all 512 columns
+      if (threadIdx.x < 32) tmem_alloc(&tslot, C::TALLOC);
       tmem_fence_before_sync();
     }
     __syncthreads();
@@ -642,7 +648,7 @@ struct Ctx {
       tmem_fence_after_sync();
       tbase = tslot;
       const int w = threadIdx.x / 32;
-      taddr = tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)((w / 4) * C::TCOLS);
+      taddr = tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)((w / 4) * C::TSTRIDE);
     }
     if constexpr (C::TWT) {  // the thread's twiddles, once for the whole kernel
       constexpr int NV = (2 * C::TWPT + 7) / 8 * 8;
@@ -660,7 +666,7 @@ struct Ctx {
     if constexpr (C::TPRIV) {
       tmem_fence_before_sync();
       __syncthreads();
-      if (threadIdx.x < 32) tmem_dealloc(tbase, 512);
+      if (threadIdx.x < 32) tmem_dealloc(tbase, C::TALLOC);
     }
   }
   __device__ __forceinline__ const double2 *vfac(long long seq, int l) const {
