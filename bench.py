@@ -25,6 +25,9 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# NCCL prints its version banner on stdout at communicator creation unless told otherwise; keep stdout to the
+# one JSON line (an explicit NCCL_DEBUG from the caller wins)
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 sys.path.insert(0, ROOT)
 
 import seeded_inputs as si  # noqa: E402
