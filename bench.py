@@ -25,9 +25,10 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-# NCCL prints its version banner on stdout at communicator creation unless told otherwise; keep stdout to the
-# one JSON line (an explicit NCCL_DEBUG from the caller wins)
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+# NCCL_DEBUG=VERSION (the GPU image's default) makes NCCL print its version banner on stdout at communicator
+# creation, ahead of the one JSON line; drop that level only (INFO/TRACE/WARN from the caller are kept)
+if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+    del os.environ["NCCL_DEBUG"]
 sys.path.insert(0, ROOT)
 
 import seeded_inputs as si  # noqa: E402
