@@ -173,7 +173,13 @@ struct Cfg {
   static constexpr bool SPLITX = R >= 32 && (!TPRIV || JT_SPLITX_TPRIV);
 
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
-  static constexpr int REGS = R >= 32 ? 255 : (PRIV ? (INV ? JT_REGS16 : JT_REGS16F) : (MAXR > 2 ? 200 : 168));
+#ifndef JT_REGS16M4
+#define JT_REGS16M4 168
+#endif
+  // (MAXR = 4: twice the row accumulators / bin rows per thread)
+  static constexpr int REGS = R >= 32 ? 255
+                                      : (PRIV ? (MAXR > 2 ? JT_REGS16M4 : (INV ? JT_REGS16 : JT_REGS16F))
+                                              : (MAXR > 2 ? 200 : 168));
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;

@@ -24,7 +24,7 @@ def child(lib, configs, reps, k0=None):
     P = ctypes.c_void_p
     L.jt_plan.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                           ctypes.c_double, ctypes.c_void_p]
-    for f in ("jt_forward", "jt_inverse"):
+    for f in ("jt_forward", "jt_inverse", "jt_adjoint"):
         getattr(L, f).argtypes = [P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     L.jt_destroy.argtypes = [P]
     out = {}
@@ -41,11 +41,20 @@ def child(lib, configs, reps, k0=None):
                 _fields_ = [("seed", ctypes.c_uint64), ("k0", ctypes.c_int), ("rmax_init", ctypes.c_int),
                             ("q", ctypes.c_int), ("sweeps", ctypes.c_int), ("device", ctypes.c_int)]
             opts = ctypes.byref(O(0, k0, 0, 3, 2, -1))
-        assert L.jt_plan(ctypes.byref(h), d, n, a, b, c["eps"], opts) == 0
+        pts = si.config_points(c)
+        if pts is None and c.get("kind", 0) == 0:
+            assert L.jt_plan(ctypes.byref(h), d, n, a, b, c["eps"], opts) == 0
+        else:  # nonuniform / second kind: jt_plan_ex (include/jt.h)
+            L.jt_plan_ex.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
+            keep = [np.ascontiguousarray(q, dtype=np.float64) for q in pts] if pts is not None else []
+            arr = (ctypes.c_void_p * d)(*[q.ctypes.data for q in keep]) if pts is not None else None
+            assert L.jt_plan_ex(ctypes.byref(h), d, n, a, b, arr, c.get("kind", 0), c["eps"], opts) == 0
         x = torch.from_numpy(si.gaussian(c["n"], 0)).cuda()
         y = torch.empty_like(x)
         s = torch.cuda.current_stream().cuda_stream
-        for fn in ("jt_forward", "jt_inverse"):
+        fns = ("jt_forward", "jt_inverse") if (pts is None and c.get("kind", 0) == 0) else ("jt_forward", "jt_adjoint")
+        for fn in fns:
             f = getattr(L, fn)
             for _ in range(3):
                 f(h, x.data_ptr(), y.data_ptr(), s)
