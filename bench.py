@@ -308,6 +308,11 @@ def main():
                     "per_axis_ms_launch_order": [round(float(v), 4) for v in per_axis_ms],
                     "hbm_algorithmic_GBps": hbm_bytes / (per_axis_ms[i_dom] * 1e-3) / 1e9,
                     "hbm_frac_of_measured": hbm_bytes / (per_axis_ms[i_dom] * 1e-3) / 1e9 / load_peaks()["hbm_gbs"],
+                    # SURVEY.md §8(d) "north-star model": the HBM traffic an unfused one-rank-term-per-pass schedule
+                    # would move (24 B per point per term: read input, read + write the accumulator) over the
+                    # measured step time, as a fraction of the measured HBM bandwidth (a fusion gain; may exceed 1)
+                    "north_star_hbm_model_frac": 24.0 * total_points * sum(ranks) / (ms_step * 1e-3) / 1e9
+                                                 / load_peaks()["hbm_gbs"],
                     "peak_source": "FP64 DFMA measured 37.0 TF/s burst = sustained (profiles/fp64_peak_r01.json); "
                                    "148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 derived"}
 
