@@ -146,6 +146,13 @@ jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, 
 jt_status jt_axis_pass(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
                        int64_t inner, int in_split, int out_split, void *cuda_stream);
 
+/* jt_axis_pass over PART of the rows of a chunk-major array: the chunk-major blocks have ostride >= outer
+ * rows (element (o, j, i) at (j / c) * (ostride * c * inner) + o * c * inner + (j % c) * inner + i); pass
+ * `out` (or `in`) already offset to the first row of the part.  Used to pipeline the distributed forward's
+ * all-to-all with its axis-1 pass.  ostride < outer is JT_ERR_ARG. */
+jt_status jt_axis_pass_ex(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
+                          int64_t inner, int in_split, int out_split, int64_t ostride, void *cuda_stream);
+
 /* ---- slab-distributed plans ----
  * One process per GPU.  Rank 0 calls jt_dist_unique_id and broadcasts the 128-byte id (e.g. over the
  * torch process group); every rank then calls jt_plan_dist with the same n, a, b, eps, opts.  The library

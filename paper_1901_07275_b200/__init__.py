@@ -34,7 +34,7 @@ _STATUS = {0: "JT_OK", 1: "JT_ERR_ARG", 2: "JT_ERR_DOMAIN", 3: "JT_ERR_NUMERIC",
 EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_kind", "jt_dist_unique_id",
             "jt_plan_dist", "jt_local_box", "jt_forward_host_async", "jt_inverse_host_async", "jt_host_wait",
             "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
-            "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_destroy", "jt_plan_rank", "jt_plan_info",
+            "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_axis_pass_ex", "jt_destroy", "jt_plan_rank", "jt_plan_info",
             "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_error", "jt_version",
             "jt_debug_modified_pq"]
 
@@ -72,6 +72,8 @@ for _f in ("jt_forward_axis", "jt_inverse_axis"):
                                   ctypes.c_int64, ctypes.c_void_p]
 _lib.jt_axis_pass.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                               ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+_lib.jt_axis_pass_ex.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                 ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p]
 _lib.jt_destroy.argtypes = [_P]
 _lib.jt_plan_rank.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
 _lib.jt_plan_info.argtypes = [_P, ctypes.c_int, _I64, _I64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
@@ -249,6 +251,13 @@ def jt_axis_pass(plan: int, axis: int, inverse: bool, x_in, x_out, outer: int, i
     """One axis pass with optional chunk-major (all-to-all) input / output layouts (include/jt.h)."""
     _check(_lib.jt_axis_pass(plan, axis, int(bool(inverse)), _ptr(x_in), _ptr(x_out), outer, inner, in_split,
                              out_split, _stream_handle(stream)), "jt_axis_pass")
+
+
+def jt_axis_pass_ex(plan: int, axis: int, inverse: bool, x_in, x_out, outer: int, inner: int, in_split: int,
+                    out_split: int, ostride: int, stream=None):
+    """jt_axis_pass over part of the rows of a chunk-major array (include/jt.h)."""
+    _check(_lib.jt_axis_pass_ex(plan, axis, int(bool(inverse)), _ptr(x_in), _ptr(x_out), outer, inner, in_split,
+                                out_split, ostride, _stream_handle(stream)), "jt_axis_pass_ex")
 
 
 def jt_destroy(plan: int):

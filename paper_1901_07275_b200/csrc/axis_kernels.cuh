@@ -749,6 +749,8 @@ __device__ __forceinline__ void load_rows(const double *__restrict__ p, int stri
 struct Layout {
   long long outer, inner;
   int in_cs, out_cs;  // chunk length of the input / output along the axis (== n: plain C-order)
+  long long ostride;  // outer extent of the chunk-major blocks (== outer, or the whole slab when a launch
+                      // covers only part of its rows: the pipelined all-to-all of the distributed forward)
 };
 
 
@@ -762,7 +764,7 @@ struct LineAddr {
     inner = inner_;
     cs = SPLIT ? cs_ : n;
     b0 = o * (long long)cs * inner_ + i;
-    cstride = SPLIT ? outer * (long long)cs * inner_ : 0;
+    cstride = SPLIT ? outer * (long long)cs * inner_ : 0;  // outer = Layout::ostride (see the kernels)
   }
   __device__ __forceinline__ long long at(int j) const {
     if constexpr (SPLIT) return b0 + (long long)(j / cs) * cstride + (long long)(j % cs) * inner;
@@ -793,8 +795,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr<SPLIT> ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
-    const LineAddr<SPLIT> oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs);
 
     // coefficients at the first-pass input positions k = vt + r TPL; degrees < k0 also to alow
     // (all loads issued before any shared-memory store, so that their latencies overlap)
@@ -927,8 +929,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr<SPLIT> ia(live ? L : 0, lay.outer, lay.inner, n, lay.in_cs);
-    const LineAddr<SPLIT> oa(live ? L : 0, lay.outer, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs);
 
     State<C, NB * MAXR> yb(cx.priv, cx.gt, cx.taddr);  // element q MAXR + c: row c of input bin q
     {

@@ -120,6 +120,8 @@ struct jt_plan_s {
   int rank = 0, nranks = 1;
   nccl::Comm comm = nullptr;
   double *a2a_send = nullptr, *a2a_recv = nullptr;
+  mutable cudaStream_t s_comm = nullptr;  // the pipelined all-to-all's stream (created on first use)
+  mutable cudaEvent_t ev_chunk[8] = {}, ev_comm = nullptr;
 };
 
 namespace {
@@ -231,12 +233,13 @@ jt_status launch_n(const jt_plan_s *p, bool inverse, int maxr, const jtk::AxisDe
 // layout of the slab all-to-all for the input / output.
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
                       long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
-                      long long nlines_only = -1, bool allow_ts = true) {
+                      long long nlines_only = -1, bool allow_ts = true, long long ostride = -1) {
   jtk::AxisDev ax = axis_dev(p, axis);
   const int maxr = p->dev[axis].maxr;
   // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
   const long long nlines = nlines_only >= 0 ? nlines_only : outer * inner;
-  const jtk::Layout lay{outer, inner, (int)(p->n[axis] / in_split), (int)(p->n[axis] / out_split)};
+  const jtk::Layout lay{outer, inner, (int)(p->n[axis] / in_split), (int)(p->n[axis] / out_split),
+                        ostride >= 0 ? ostride : outer};
   switch (ax.N) {
     case 16: return launch_n<16>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
     case 32: return launch_n<32>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
@@ -289,6 +292,10 @@ void free_device(jt_plan_s *p) {
   cudaFree(p->a2a_recv);
   p->a2a_send = p->a2a_recv = nullptr;
   if (p->comm) nccl::api().CommDestroy(p->comm), p->comm = nullptr;
+  for (auto &e : p->ev_chunk)
+    if (e) cudaEventDestroy(e), e = nullptr;
+  if (p->ev_comm) cudaEventDestroy(p->ev_comm), p->ev_comm = nullptr;
+  if (p->s_comm) cudaStreamDestroy(p->s_comm), p->s_comm = nullptr;
   for (auto &e : p->ev)
     if (e) cudaEventDestroy(e), e = nullptr;
   if (p->s_h2d) cudaStreamDestroy(p->s_h2d), p->s_h2d = nullptr;
@@ -396,19 +403,59 @@ jt_status all_to_all(const jt_plan_s *p, cudaStream_t s) {
 // Slab schedule of a distributed plan (the C twin of paper_1901_07275_b200/dist.py SlabPlan):
 //   forward: axes d-1..1 on the x-slab (axis 1 written chunk-major), all-to-all, axis 0 on the y-slab;
 //   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major.
+// All-to-all of the rows [r0, r1) of every rank's chunk-major blocks (a piece of each of the G blocks of CH
+// doubles: rows of `rowlen` doubles), on stream s.
+jt_status all_to_all_rows(const jt_plan_s *p, long long r0, long long r1, long long rowlen, cudaStream_t s) {
+  nccl::Api &A = nccl::api();
+  const size_t chunk = (size_t)p->total / p->nranks;
+  const size_t off = (size_t)(r0 * rowlen), cnt = (size_t)((r1 - r0) * rowlen);
+  int e = A.GroupStart();
+  for (int g = 0; g < p->nranks && e == nccl::Success; ++g) {
+    e = A.Send(p->a2a_send + g * chunk + off, cnt, nccl::Float64, g, p->comm, s);
+    if (e == nccl::Success) e = A.Recv(p->a2a_recv + g * chunk + off, cnt, nccl::Float64, g, p->comm, s);
+  }
+  const int e2 = A.GroupEnd();
+  if (e != nccl::Success || e2 != nccl::Success)
+    return fail(JT_ERR_NCCL, std::string("all-to-all: ") + A.GetErrorString(e != nccl::Success ? e : e2));
+  return JT_OK;
+}
+
+// Slab schedule of a distributed plan (the C twin of paper_1901_07275_b200/dist.py SlabPlan):
+//   forward: axes d-1..1 on the x-slab (axis 1 written chunk-major), all-to-all, axis 0 on the y-slab; the
+//            axis-1 pass and the all-to-all are pipelined over KA row chunks of the slab: chunk k's rows are
+//            sent (comm stream) while chunk k+1's axis-1 pass computes;
+//   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major.
 jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   const int G = p->nranks, d = p->d;
   const long long n0 = p->n[0], n1 = p->n[1], r = d == 3 ? p->n[2] : 1;
   jt_status st;
   if (!inverse) {
+    const long long R = n0 / G, c = n1 / G;  // slab rows, chunk length of axis 1
+    const double *src1 = in;
     if (d == 3) {
-      if ((st = launch_axis(p, 2, false, in, out, (n0 / G) * n1, 1, s)) != JT_OK) return st;
-      if ((st = launch_axis(p, 1, false, out, p->a2a_send, n0 / G, r, s, 1, G)) != JT_OK) return st;
-    } else if ((st = launch_axis(p, 1, false, in, p->a2a_send, n0 / G, 1, s, 1, G)) != JT_OK) {
-      return st;
+      if ((st = launch_axis(p, 2, false, in, out, R * n1, 1, s)) != JT_OK) return st;
+      src1 = out;
     }
-    if ((st = all_to_all(p, s)) != JT_OK) return st;
-    return launch_axis(p, 0, false, p->a2a_recv, out, 1, (n1 / G) * r, s);
+    if (!p->s_comm) {
+      JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
+      for (auto &e : p->ev_chunk) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      JT_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_comm, cudaEventDisableTiming));
+    }
+    const int KA = (int)std::min<long long>(4, R);  // (also at G = 1: the self-exchange path is exercised)
+    for (int k = 0; k < KA; ++k) {
+      const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
+      if (r1 == r0) continue;
+      // rows [r0, r1) of the slab: input rows r0.., output rows r0.. of every chunk-major block
+      if ((st = launch_axis(p, 1, false, src1 + r0 * n1 * r, p->a2a_send + r0 * c * r, r1 - r0, r, s, 1, G, -1, true,
+                            R)) != JT_OK)
+        return st;
+      JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], s));
+      JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_chunk[k], 0));
+      if ((st = all_to_all_rows(p, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
+    }
+    JT_CUDA_TRY(cudaEventRecord(p->ev_comm, p->s_comm));
+    JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
+    return launch_axis(p, 0, false, p->a2a_recv, out, 1, c * r, s);
   }
   if (d == 3) {
     if ((st = launch_axis(p, 2, true, in, out, n0 * (n1 / G), 1, s)) != JT_OK) return st;
@@ -697,7 +744,7 @@ jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs
 }
 
 static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *in, double *out, int64_t outer,
-                            int64_t inner, int in_split, int out_split, void *stream) {
+                            int64_t inner, int in_split, int out_split, void *stream, int64_t ostride = -1) {
   jt_status st = check_device_plan(p);
   if (st != JT_OK) return st;
   if (axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad axis");
@@ -709,7 +756,9 @@ static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *i
   if (in == out && (in_split != 1 || out_split != 1))
     return fail(JT_ERR_ARG, "chunk-major layouts need out-of-place buffers");
   DeviceGuard g(p->device);
-  return launch_axis(p, axis, inverse, in, out, outer, inner, (cudaStream_t)stream, in_split, out_split);
+  if (ostride >= 0 && ostride < outer) return fail(JT_ERR_ARG, "ostride must be >= outer");
+  return launch_axis(p, axis, inverse, in, out, outer, inner, (cudaStream_t)stream, in_split, out_split, -1, true,
+                     ostride);
 }
 
 jt_status jt_forward_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer, int64_t inner,
@@ -725,6 +774,11 @@ jt_status jt_inverse_axis(jt_plan_t p, int axis, const double *in, double *out, 
 jt_status jt_axis_pass(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
                        int64_t inner, int in_split, int out_split, void *stream) {
   return axis_entry(p, axis, inverse != 0, in, out, outer, inner, in_split, out_split, stream);
+}
+
+jt_status jt_axis_pass_ex(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
+                          int64_t inner, int in_split, int out_split, int64_t ostride, void *stream) {
+  return axis_entry(p, axis, inverse != 0, in, out, outer, inner, in_split, out_split, stream, ostride);
 }
 
 jt_status jt_dist_unique_id(void *nccl_unique_id) {

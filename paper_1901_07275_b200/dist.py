@@ -53,13 +53,14 @@ class SlabPlan:
         self.count = int(np.prod(self.x_shape))
         self.plan = None
         if axis_pass is None:
-            from . import Plan, jt_axis_pass
+            from . import Plan, jt_axis_pass_ex
             self.plan = Plan(self.shape, a, b, eps, **plan_kw)
             self.ranks = [self.plan.rank(i) for i in range(self.d)]
             handle = self.plan.handle
 
-            def axis_pass(axis, inverse, src, dst, outer, inner, in_split, out_split):
-                jt_axis_pass(handle, axis, inverse, src, dst, outer, inner, in_split, out_split)
+            def axis_pass(axis, inverse, src, dst, outer, inner, in_split, out_split, ostride=None):
+                jt_axis_pass_ex(handle, axis, inverse, src, dst, outer, inner, in_split, out_split,
+                                outer if ostride is None else ostride)
             self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         else:
             self.ranks = None
@@ -98,11 +99,47 @@ class SlabPlan:
         self.dist.all_to_all_single(self._recv, self._send, group=self.group)
 
     # ---- transforms ----
-    def forward(self, x, out=None):
-        """x-slab coefficients -> y-slab weighted values (the local block of Phi_0 (x) ... (x) Phi_{d-1} alpha)."""
-        out = self.forward_local(x, out)
-        self._exchange()
+    def forward(self, x, out=None, chunks=None):
+        """x-slab coefficients -> y-slab weighted values (the local block of Phi_0 (x) ... (x) Phi_{d-1} alpha).
+
+        The axis-1 pass and the all-to-all are pipelined over `chunks` row chunks of the slab (default
+        min(4, rows), the same as the library's transform_dist): chunk k's rows of every chunk-major block are
+        exchanged (point-to-point) after its axis-1 pass."""
+        import torch
+        if tuple(x.shape) != self.x_shape:
+            raise ValueError(f"expected the x-slab shape {self.x_shape}")
+        out = torch.empty(self.y_shape, dtype=torch.float64, device=self.device) if out is None else out
+        G, (n0, n1), r = self.G, self.shape[:2], self.rest
+        R, c = n0 // G, n1 // G
+        K = chunks if chunks is not None else min(4, R)
+        src = x
+        if self.d == 3:
+            self._axis(2, False, x, out, R * n1, 1, 1, 1)
+            src = out
+        flat_src = src.reshape(-1)
+        for k in range(K):
+            r0, r1 = R * k // K, R * (k + 1) // K
+            if r1 == r0:
+                continue
+            self._axis(1, False, flat_src[r0 * n1 * r:r1 * n1 * r], self._send[r0 * c * r:], r1 - r0, r, 1, G,
+                       ostride=R)
+            self._exchange_rows(r0, r1, c * r)
         return self.forward_finish(out)
+
+    def _exchange_rows(self, r0, r1, rowlen):
+        """Rows [r0, r1) of every chunk-major block to / from every rank (point-to-point)."""
+        CH = self.count // self.G
+        reqs = []
+        for g in range(self.G):
+            s_view = self._send[g * CH + r0 * rowlen:g * CH + r1 * rowlen]
+            r_view = self._recv[g * CH + r0 * rowlen:g * CH + r1 * rowlen]
+            if g == self.rank:
+                r_view.copy_(s_view)
+            else:
+                reqs.append(self.dist.isend(s_view, g, group=self.group))
+                reqs.append(self.dist.irecv(r_view, g, group=self.group))
+        for q in reqs:
+            q.wait()
 
     def forward_local(self, x, out=None):
         """Forward phase 1: the local axis passes d-1 .. 1; leaves the chunk-major send buffer filled."""

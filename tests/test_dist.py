@@ -21,28 +21,30 @@ import seeded_inputs as si
 torch = pytest.importorskip("torch")
 
 
-def chunk_index(outer, n, inner, split):
+def chunk_index(outer, n, inner, split, ostride=None):
     """Flat positions of element (o, j, i) of an (outer, n, inner) array in the chunk-major layout
-    (include/jt.h jt_axis_pass): (j / c) (outer c inner) + o c inner + (j % c) inner + i, c = n / split."""
+    (include/jt.h jt_axis_pass / jt_axis_pass_ex): (j / c) (ostride c inner) + o c inner + (j % c) inner + i,
+    c = n / split, ostride = outer unless the launch covers part of the rows."""
     c = n // split
+    ostride = outer if ostride is None else ostride
     o = np.arange(outer)[:, None, None]
     j = np.arange(n)[None, :, None]
     i = np.arange(inner)[None, None, :]
-    return (j // c) * (outer * c * inner) + o * c * inner + (j % c) * inner + i
+    return (j // c) * (ostride * c * inner) + o * c * inner + (j % c) * inner + i
 
 
 def make_oracle_axis_pass(shape, a, b):
     mats = [oracle.phi(shape[ax], a[ax], b[ax]) for ax in range(len(shape))]
 
-    def axis_pass(axis, inverse, src, dst, outer, inner, in_split, out_split):
+    def axis_pass(axis, inverse, src, dst, outer, inner, in_split, out_split, ostride=None):
         n = shape[axis]
         M = mats[axis].T if inverse else mats[axis]
         s = src.reshape(-1).numpy()
-        X = s[chunk_index(outer, n, inner, in_split)]            # (outer, n, inner)
+        X = s[chunk_index(outer, n, inner, in_split, ostride if in_split > 1 else None)]   # (outer, n, inner)
         Y = np.einsum("jk,okI->ojI", M, X)
-        out = np.empty(outer * n * inner)
-        out[chunk_index(outer, n, inner, out_split)] = Y
-        dst.reshape(-1).copy_(torch.from_numpy(out))
+        d = dst.reshape(-1)
+        idx = chunk_index(outer, n, inner, out_split, ostride if out_split > 1 else None)
+        d[torch.from_numpy(idx.ravel())] = torch.from_numpy(Y.ravel())
     return axis_pass
 
 
