@@ -385,26 +385,22 @@ jt_status check_device_plan(const jt_plan_s *p) {
 }
 
 // Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
-// One all-to-all of equal contiguous chunks (send chunk g to rank g) on stream s.
-jt_status all_to_all(const jt_plan_s *p, cudaStream_t s) {
-  nccl::Api &A = nccl::api();
-  const size_t chunk = (size_t)p->total / p->nranks;
-  int e = A.GroupStart();
-  for (int g = 0; g < p->nranks && e == nccl::Success; ++g) {
-    e = A.Send(p->a2a_send + g * chunk, chunk, nccl::Float64, g, p->comm, s);
-    if (e == nccl::Success) e = A.Recv(p->a2a_recv + g * chunk, chunk, nccl::Float64, g, p->comm, s);
+
+jt_status ensure_comm_stream(const jt_plan_s *p) {
+  if (!p->s_comm) {
+    JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
+    for (auto &e : p->ev_chunk) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    JT_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_comm, cudaEventDisableTiming));
   }
-  const int e2 = A.GroupEnd();
-  if (e != nccl::Success || e2 != nccl::Success)
-    return fail(JT_ERR_NCCL, std::string("all-to-all: ") + A.GetErrorString(e != nccl::Success ? e : e2));
   return JT_OK;
 }
 
 // Slab schedule of a distributed plan (the C twin of paper_1901_07275_b200/dist.py SlabPlan):
 //   forward: axes d-1..1 on the x-slab (axis 1 written chunk-major), all-to-all, axis 0 on the y-slab;
-//   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major.
-// All-to-all of the rows [r0, r1) of every rank's chunk-major blocks (a piece of each of the G blocks of CH
-// doubles: rows of `rowlen` doubles), on stream s.
+//   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major; the
+//            all-to-all and the axis-1 pass are pipelined over KA row chunks of the x-slab (receiver side).
+// All-to-all of rows [r0, r1) (rowlen elements each) of every contiguous chunk-major block (block g to /
+// from rank g) on stream s; the whole exchange is r0 = 0, r1 = rows per block.
 jt_status all_to_all_rows(const jt_plan_s *p, long long r0, long long r1, long long rowlen, cudaStream_t s) {
   nccl::Api &A = nccl::api();
   const size_t chunk = (size_t)p->total / p->nranks;
@@ -424,7 +420,8 @@ jt_status all_to_all_rows(const jt_plan_s *p, long long r0, long long r1, long l
 //   forward: axes d-1..1 on the x-slab (axis 1 written chunk-major), all-to-all, axis 0 on the y-slab; the
 //            axis-1 pass and the all-to-all are pipelined over KA row chunks of the slab: chunk k's rows are
 //            sent (comm stream) while chunk k+1's axis-1 pass computes;
-//   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major.
+//   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major; the
+//            all-to-all and the axis-1 pass are pipelined over KA row chunks of the x-slab (receiver side).
 jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   const int G = p->nranks, d = p->d;
   const long long n0 = p->n[0], n1 = p->n[1], r = d == 3 ? p->n[2] : 1;
@@ -436,11 +433,7 @@ jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, dou
       if ((st = launch_axis(p, 2, false, in, out, R * n1, 1, s)) != JT_OK) return st;
       src1 = out;
     }
-    if (!p->s_comm) {
-      JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
-      for (auto &e : p->ev_chunk) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      JT_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_comm, cudaEventDisableTiming));
-    }
+    if ((st = ensure_comm_stream(p)) != JT_OK) return st;
     const int KA = (int)std::min<long long>(4, R);  // (also at G = 1: the self-exchange path is exercised)
     for (int k = 0; k < KA; ++k) {
       const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
@@ -457,14 +450,29 @@ jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, dou
     JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
     return launch_axis(p, 0, false, p->a2a_recv, out, 1, c * r, s);
   }
+  const long long R = n0 / G, c = n1 / G;
   if (d == 3) {
-    if ((st = launch_axis(p, 2, true, in, out, n0 * (n1 / G), 1, s)) != JT_OK) return st;
-    if ((st = launch_axis(p, 0, true, out, p->a2a_send, 1, (n1 / G) * r, s, 1, G)) != JT_OK) return st;
-  } else if ((st = launch_axis(p, 0, true, in, p->a2a_send, 1, n1 / G, s, 1, G)) != JT_OK) {
+    if ((st = launch_axis(p, 2, true, in, out, n0 * c, 1, s)) != JT_OK) return st;
+    if ((st = launch_axis(p, 0, true, out, p->a2a_send, 1, c * r, s, 1, G)) != JT_OK) return st;
+  } else if ((st = launch_axis(p, 0, true, in, p->a2a_send, 1, c, s, 1, G)) != JT_OK) {
     return st;
   }
-  if ((st = all_to_all(p, s)) != JT_OK) return st;
-  return launch_axis(p, 1, true, p->a2a_recv, out, n0 / G, r, s, G, 1);
+  if ((st = ensure_comm_stream(p)) != JT_OK) return st;
+  JT_CUDA_TRY(cudaEventRecord(p->ev_comm, s));
+  JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_comm, 0));
+  // the exchange in KA row chunks of the x-slab on the comm stream; chunk k's axis-1 pass waits for its rows only
+  const int KA = (int)std::min<long long>(4, R);
+  for (int k = 0; k < KA; ++k) {
+    const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
+    if (r1 == r0) continue;
+    if ((st = all_to_all_rows(p, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
+    JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], p->s_comm));
+    JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_chunk[k], 0));
+    if ((st = launch_axis(p, 1, true, p->a2a_recv + r0 * c * r, out + r0 * n1 * r, r1 - r0, r, s, G, 1, -1, true,
+                          R)) != JT_OK)
+      return st;
+  }
+  return JT_OK;
 }
 
 jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {

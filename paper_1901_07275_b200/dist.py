@@ -161,11 +161,25 @@ class SlabPlan:
         self._axis(0, False, self._recv, out, 1, (n1 // G) * r, 1, 1)
         return out
 
-    def inverse(self, y, out=None):
-        """y-slab weighted values -> x-slab coefficients (transpose in every axis)."""
+    def inverse(self, y, out=None, chunks=None):
+        """y-slab weighted values -> x-slab coefficients (transpose in every axis).
+
+        The all-to-all and the axis-1 pass are pipelined over `chunks` row chunks of the x-slab (default
+        min(4, rows), as in the library's transform_dist): rows [r0, r1) of every block are exchanged, then the
+        axis-1 pass runs on those rows while the next chunk is in flight."""
         out = self.inverse_local(y, out)
-        self._exchange()
-        return self.inverse_finish(out)
+        G, (n0, n1), r = self.G, self.shape[:2], self.rest
+        R, c = n0 // G, n1 // G
+        K = chunks if chunks is not None else min(4, R)
+        flat_out = out.reshape(-1)
+        for k in range(K):
+            r0, r1 = R * k // K, R * (k + 1) // K
+            if r1 == r0:
+                continue
+            self._exchange_rows(r0, r1, c * r)
+            self._axis(1, True, self._recv[r0 * c * r:], flat_out[r0 * n1 * r:r1 * n1 * r], r1 - r0, r, G, 1,
+                       ostride=R)
+        return out
 
     def inverse_local(self, y, out=None):
         """Inverse phase 1: axis d-1 pass, axis-0 pass into the chunk-major send buffer."""
