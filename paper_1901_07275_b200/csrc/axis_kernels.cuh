@@ -66,6 +66,11 @@ struct TermSplit {
   double *part;
 };
 
+// unroll factor of the batch-start W V loops (N > 512: all k0 degrees there, rows read through L1)
+#ifndef JT_VUNROLL
+#define JT_VUNROLL 4  // (the loads of 4 degrees in flight: N = 4096 forward -7 %, N = 2048 inverse -7 %)
+#endif
+
 constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
 constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
                             // (4 measured slower: a bigger stage leaves room for only 2 ring stages)
@@ -192,6 +197,7 @@ struct Cfg {
   // layout [m][c][kk], so the dense low-degree block is applied inside the term loop from SMEM]
   static constexpr bool STAGED = N <= 1024;
   static constexpr bool VST = N <= 512;
+  static constexpr int VUN = VST ? 1 : JT_VUNROLL;  // unroll of the batch-start W V loops
   static constexpr int KPT = VST ? VST_KPT : 0;
   static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
   static constexpr int STAGE_BYTES = STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : 0;
@@ -207,7 +213,26 @@ struct Cfg {
 #ifndef JT_TWT_INV32
 #define JT_TWT_INV32 0
 #endif
-  static constexpr bool TWT = TWS && TPRIV && JT_TWT && TWPT > 0 && MAXR == 2 && (!INV || R == 16 || JT_TWT_INV32);
+#ifndef JT_TWT_LARGE
+#define JT_TWT_LARGE 1
+#endif
+// twiddles per TMEM wait in the N > 1024 passes (measured: forward 4 -5 % vs 8 at N = 4096; inverse 8 -3 % at 2048)
+#ifndef JT_TWT_CH_LARGE_F
+#define JT_TWT_CH_LARGE_F 4
+#endif
+#ifndef JT_TWT_CH_LARGE_I
+#define JT_TWT_CH_LARGE_I 8
+#endif
+#ifndef JT_TWT_LARGE_INV_NMAX
+#define JT_TWT_LARGE_INV_NMAX 2048  // (the N = 4096 inverse measured 1 % slower with it, N = 2048 2 % faster)
+#endif
+  // N > 1024 (no SMEM table, TWS off): the twiddles in TMEM too, one copy per lane quadrant shared by the warps
+  // of that quadrant (TW_SHARED: warps w and w + 4 have the same thread positions vt when the group size
+  // divides 128), after all the warps' state slices
+  static constexpr bool TWT_LARGE = !TWS && JT_TWT_LARGE && 128 % GT == 0 && (!INV || N <= JT_TWT_LARGE_INV_NMAX);
+  static constexpr bool TWT = (TWS || TWT_LARGE) && TPRIV && JT_TWT && TWPT > 0 && MAXR == 2 &&
+                              (!INV || R == 16 || JT_TWT_INV32 || !TWS);
+  static constexpr bool TW_SHARED = TWT && !TWS;
   static constexpr int TW_BYTES = (TWS && !TWT) ? (TwTotal<N, R>::value * 16 + 127) / 128 * 128 : 0;
   // per-CTA table of the row range of every (thread position vt, bin slot q): (j0 << 4) | count
   static constexpr int BINFO_BYTES = STAGED ? (TPL * NB * 4 + 127) / 128 * 128 : 0;
@@ -239,12 +264,17 @@ struct Cfg {
   static constexpr int TW_COL0 = (PSTATE + 15) / 16 * 32;          // twiddles after the state chunks
   static constexpr int TW_COLS = TWT ? (4 * TWPT + 31) / 32 * 32 : 0;
   static constexpr int pow2_ge(int v, int p = 32) { return p >= v ? p : pow2_ge(v, 2 * p); }
+  static constexpr int WPQ = (NWARP + 3) / 4;  // warps per lane quadrant
+  // columns of a quadrant: WPQ slices [state | own twiddles], or (TW_SHARED) WPQ state slices + one twiddle copy
+  // (+32: a butterfly's twiddle loads are whole 8-complex chunks and may read past the last one)
+  static constexpr int TUSED = TW_SHARED ? WPQ * TW_COL0 + TW_COLS + 32 : (TW_COL0 + TW_COLS) * WPQ;
   // allocate only what the slices use (a power of two >= 32), so CTAs that co-reside on an SM can all allocate
-  static constexpr int TALLOC = pow2_ge((TW_COL0 + TW_COLS) * ((NWARP + 3) / 4) > 512 ? 512
-                                                                                    : (TW_COL0 + TW_COLS) * ((NWARP + 3) / 4));
-  static constexpr int TSTRIDE = TALLOC / ((NWARP + 3) / 4) / 16 * 16;
-  static constexpr bool TMEM_OK = !TPRIV || (NWARP % 4 == 0 && TW_COL0 + TW_COLS <= TCOLS);
-  static_assert(!TPRIV || TW_COL0 + TW_COLS <= TSTRIDE, "TMEM slice stride");
+  static constexpr int TALLOC = pow2_ge(TUSED > 512 ? 512 : TUSED);
+  static constexpr int TSTRIDE = TW_SHARED ? TW_COL0 : TALLOC / WPQ / 16 * 16;
+  static constexpr int TW_BASE = TW_SHARED ? WPQ * TW_COL0 : TW_COL0;  // twiddles: from the quadrant / slice base
+  static constexpr bool TMEM_OK =
+      !TPRIV || (NWARP % 4 == 0 && (TW_SHARED ? TUSED <= 512 : TW_COL0 + TW_COLS <= TCOLS));
+  static_assert(!TPRIV || TW_SHARED || TW_COL0 + TW_COLS <= TSTRIDE, "TMEM slice stride");
 #ifndef JT_NO_TMEM_ASSERT
   static_assert(TMEM_OK, "TMEM state slice");
 #endif
@@ -407,64 +437,93 @@ __device__ __forceinline__ void pass_compute(double (&xr)[C::R], double (&xi)[C:
                                              const double2 *__restrict__ tw, uint32_t ttw) {
   using P = Pass<C::N, C::R, NS>;
   constexpr int RS = P::RS;
+  if constexpr (C::TW_SHARED) {
+    // this thread's twiddles of the pass (butterfly i, r = 1..RS-1, consecutive in TMEM), TCH complex per wait
+    // across butterfly boundaries (the radix-2 / radix-4 last passes of N > 1024 have 1 / 3 per butterfly),
+    // then the DFTs
+    constexpr int NTW = P::B * (RS - 1);
+    constexpr int TCH = C::INV ? JT_TWT_CH_LARGE_I : JT_TWT_CH_LARGE_F;
+    const uint32_t t0 = ttw + 4 * TwPrefix<C::N, C::R, NS>::value;
 #pragma unroll
-  for (int i = 0; i < P::B; ++i) {
-    const int v = vt + i * C::TPL;
-    if constexpr (C::TWT) {
-      // this thread's twiddles w^r, r = 1..RS-1, from its TMEM slice, 8 complex per tcgen05.ld pair
-      constexpr int NCHK = (RS - 1 + 7) / 8;
-      const uint32_t t0 = ttw + 4 * (TwPrefix<C::N, C::R, NS>::value + i * (RS - 1));
+    for (int ch = 0; ch < (NTW + TCH - 1) / TCH; ++ch) {
+      double w[16];
+      tmem_ld_d8(t0 + 4 * TCH * ch, &w[0]);
+      if constexpr (TCH == 8) tmem_ld_d8(t0 + 4 * TCH * ch + 16, &w[8]);
+      tmem_wait_ld();
 #pragma unroll
-      for (int ch = 0; ch < NCHK; ++ch) {
-        double w[16];
-        tmem_ld_d8(t0 + 32 * ch, &w[0]);
-        tmem_ld_d8(t0 + 32 * ch + 16, &w[8]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int r = 1 + 8 * ch + j;
-          if (r < RS) {
-            const double pr = w[2 * j], pim = w[2 * j + 1];
-            const double tr = xr[i * RS + r] * pr - xi[i * RS + r] * pim;
-            xi[i * RS + r] = fma(xr[i * RS + r], pim, xi[i * RS + r] * pr);
-            xr[i * RS + r] = tr;
-          }
+      for (int j = 0; j < TCH; ++j) {
+        const int k = TCH * ch + j;
+        if (k < NTW) {
+          const int e = (k / (RS - 1)) * RS + 1 + k % (RS - 1);
+          const double pr = w[2 * j], pim = w[2 * j + 1];
+          const double tr = xr[e] * pr - xi[e] * pim;
+          xi[e] = fma(xr[e], pim, xi[e] * pr);
+          xr[e] = tr;
         }
       }
-      dft<RS>(&xr[i * RS], &xi[i * RS]);
-      continue;
-    }
-    // Twiddles w^r, w = e^{2 pi i (v mod NS) / (NS RS)}: every one from the SMEM table (TWS), or exact table
-    // values at the anchors r = 1 (mod 8) and the chain w^r = w^{r-1} w in between (from global / L1).
-    double pr = 1.0, pim = 0.0;
-    double2 w1;
-    const double2 *twp;
-    if constexpr (C::TWS) {
-      twp = tw_smem_base(C::TW_OFF) + TwOff<C::N, C::R, NS>::value + (v % NS);
-    } else {
-      twp = tw + TwOff<C::N, C::R, NS>::value + (v % NS);
-      w1 = __ldg(&twp[0]);
     }
 #pragma unroll
-    for (int r = 1; r < RS; ++r) {
-      if constexpr (C::TWS) {  // every twiddle from the SMEM table
-        const double2 wa = twp[(r - 1) * NS];
-        pr = wa.x;
-        pim = wa.y;
-      } else if (r % 8 == 1) {
-        const double2 wa = r == 1 ? w1 : __ldg(&twp[(r - 1) * NS]);
-        pr = wa.x;
-        pim = wa.y;
-      } else {
-        const double t = pr * w1.x - pim * w1.y;
-        pim = fma(pr, w1.y, pim * w1.x);
-        pr = t;
+    for (int i = 0; i < P::B; ++i) dft<RS>(&xr[i * RS], &xi[i * RS]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < P::B; ++i) {
+      const int v = vt + i * C::TPL;
+      if constexpr (C::TWT) {
+        // this thread's twiddles w^r, r = 1..RS-1, from its TMEM slice, 8 complex per tcgen05.ld pair
+        constexpr int NCHK = (RS - 1 + 7) / 8;
+        const uint32_t t0 = ttw + 4 * (TwPrefix<C::N, C::R, NS>::value + i * (RS - 1));
+#pragma unroll
+        for (int ch = 0; ch < NCHK; ++ch) {
+          double w[16];
+          tmem_ld_d8(t0 + 32 * ch, &w[0]);
+          tmem_ld_d8(t0 + 32 * ch + 16, &w[8]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = 1 + 8 * ch + j;
+            if (r < RS) {
+              const double pr = w[2 * j], pim = w[2 * j + 1];
+              const double tr = xr[i * RS + r] * pr - xi[i * RS + r] * pim;
+              xi[i * RS + r] = fma(xr[i * RS + r], pim, xi[i * RS + r] * pr);
+              xr[i * RS + r] = tr;
+            }
+          }
+        }
+        dft<RS>(&xr[i * RS], &xi[i * RS]);
+        continue;
       }
-      const double tr = xr[i * RS + r] * pr - xi[i * RS + r] * pim;
-      xi[i * RS + r] = fma(xr[i * RS + r], pim, xi[i * RS + r] * pr);
-      xr[i * RS + r] = tr;
+      // Twiddles w^r, w = e^{2 pi i (v mod NS) / (NS RS)}: every one from the SMEM table (TWS), or exact table
+      // values at the anchors r = 1 (mod 8) and the chain w^r = w^{r-1} w in between (from global / L1).
+      double pr = 1.0, pim = 0.0;
+      double2 w1;
+      const double2 *twp;
+      if constexpr (C::TWS) {
+        twp = tw_smem_base(C::TW_OFF) + TwOff<C::N, C::R, NS>::value + (v % NS);
+      } else {
+        twp = tw + TwOff<C::N, C::R, NS>::value + (v % NS);
+        w1 = __ldg(&twp[0]);
+      }
+#pragma unroll
+      for (int r = 1; r < RS; ++r) {
+        if constexpr (C::TWS) {  // every twiddle from the SMEM table
+          const double2 wa = twp[(r - 1) * NS];
+          pr = wa.x;
+          pim = wa.y;
+        } else if (r % 8 == 1) {
+          const double2 wa = r == 1 ? w1 : __ldg(&twp[(r - 1) * NS]);
+          pr = wa.x;
+          pim = wa.y;
+        } else {
+          const double t = pr * w1.x - pim * w1.y;
+          pim = fma(pr, w1.y, pim * w1.x);
+          pr = t;
+        }
+        const double tr = xr[i * RS + r] * pr - xi[i * RS + r] * pim;
+        xi[i * RS + r] = fma(xr[i * RS + r], pim, xi[i * RS + r] * pr);
+        xr[i * RS + r] = tr;
+      }
+      dft<RS>(&xr[i * RS], &xi[i * RS]);
     }
-    dft<RS>(&xr[i * RS], &xi[i * RS]);
   }
 }
 
@@ -554,6 +613,7 @@ template <class C, bool TSPLIT = false>
 struct Ctx {
   int grp, gt, line, vt;
   uint32_t tbase = 0, taddr = 0;  // TMEM allocation base / this thread's state slice (C::TPRIV)
+  uint32_t ttw = 0;               // this thread's twiddles (C::TWT)
   void *buf;     // group exchange buffer
   double *alow;  // group: k0 x LG low-degree coefficients (forward) / reduced a_V (inverse)
   double *priv;  // group: thread-private slots [slot][gt] (C::PRIV)
@@ -655,16 +715,25 @@ struct Ctx {
       tbase = tslot;
       const int w = threadIdx.x / 32;
       taddr = tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)((w / 4) * C::TSTRIDE);
+      ttw = C::TW_SHARED ? tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)C::TW_BASE : taddr + C::TW_BASE;
     }
     if constexpr (C::TWT) {  // the thread's twiddles, once for the whole kernel
-      constexpr int NV = (2 * C::TWPT + 7) / 8 * 8;
-      double t[NV];
+      // (TW_SHARED: the quadrant's first warp writes the copy; the others read it after the barrier below)
+      if (!C::TW_SHARED || threadIdx.x < 128) {
+        constexpr int NV = (2 * C::TWPT + 7) / 8 * 8;
+        double t[NV];
 #pragma unroll
-      for (int i = 2 * C::TWPT; i < NV; ++i) t[i] = 0.0;
-      tw_fill<C, Pass<C::N, C::R, 1>::RS>(t, vt, tw);
+        for (int i = 2 * C::TWPT; i < NV; ++i) t[i] = 0.0;
+        tw_fill<C, Pass<C::N, C::R, 1>::RS>(t, vt, tw);
 #pragma unroll
-      for (int c = 0; c < NV / 8; ++c) tmem_st_d8(taddr + C::TW_COL0 + 16 * c, &t[8 * c]);
-      tmem_wait_st();
+        for (int c = 0; c < NV / 8; ++c) tmem_st_d8(ttw + 16 * c, &t[8 * c]);
+        tmem_wait_st();
+      }
+      if constexpr (C::TW_SHARED) {
+        tmem_fence_before_sync();
+        __syncthreads();
+        tmem_fence_after_sync();
+      }
     }
   }
   // end of the kernel: every warp's TMEM traffic done, then warp 0 frees the allocation
@@ -823,6 +892,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int c = 0; c < MAXR; ++c) y[q][c] = 0.0;
     group_sync<C>();
+#pragma unroll C::VUN
     for (int k = kin; k < ((!TSPLIT || cx.slice == 0) ? k0 : kin); ++k) {
       const double ak = cx.alow[k * LG + line];
       const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
@@ -869,7 +939,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
           }
         }
       }
-      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.taddr + C::TW_COL0);  // A2
+      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // A2
 #pragma unroll
       for (int q = 0; q < NB; ++q) {  // A3
         const int e = fwd_reg_of_bin<C>(q);
@@ -952,6 +1022,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         for (int i = cx.gt; i < k0 * LG; i += C::GT) cx.alow[i] = 0.0;
         for (int i = cx.gt; i < kin * C::GW * LG; i += C::GT) cx.vred[i] = 0.0;
       }
+#pragma unroll C::VUN
       for (int k = kin; k < ((!TSPLIT || cx.slice == 0) ? k0 : kin); ++k) {
         const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
         double p = 0.0;
@@ -1042,7 +1113,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
           }
         }
       }
-      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.taddr + C::TW_COL0);
+      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);
 #pragma unroll
       for (int e = 0; e < R; ++e) {  // a[k] += Re(v_l[k] B[k])
         const double2 vv = vl[out_pos<C>(vt, e)];

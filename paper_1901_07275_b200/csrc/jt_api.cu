@@ -384,8 +384,7 @@ jt_status check_device_plan(const jt_plan_s *p) {
   return JT_OK;
 }
 
-// Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
-
+// Comm stream and events of the pipelined all-to-all (created on first use).
 jt_status ensure_comm_stream(const jt_plan_s *p) {
   if (!p->s_comm) {
     JT_CUDA_TRY(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
@@ -395,10 +394,6 @@ jt_status ensure_comm_stream(const jt_plan_s *p) {
   return JT_OK;
 }
 
-// Slab schedule of a distributed plan (the C twin of paper_1901_07275_b200/dist.py SlabPlan):
-//   forward: axes d-1..1 on the x-slab (axis 1 written chunk-major), all-to-all, axis 0 on the y-slab;
-//   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major; the
-//            all-to-all and the axis-1 pass are pipelined over KA row chunks of the x-slab (receiver side).
 // All-to-all of rows [r0, r1) (rowlen elements each) of every contiguous chunk-major block (block g to /
 // from rank g) on stream s; the whole exchange is r0 = 0, r1 = rows per block.
 jt_status all_to_all_rows(const jt_plan_s *p, long long r0, long long r1, long long rowlen, cudaStream_t s) {
@@ -475,6 +470,7 @@ jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, dou
   return JT_OK;
 }
 
+// Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
 jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   jt_status st = check_device_plan(p);
   if (st != JT_OK) return st;

@@ -1,6 +1,7 @@
 """A/B timing of several libjt builds on the same box (dev tool; raw ctypes so older builds load too).
 
-    python tools/ab_time.py LIB1.so LIB2.so ... [--configs cfg5_3d_512,cfg4_3d_256] [--reps 20] [--rounds 2]
+    python tools/ab_time.py LIB1.so LIB2.so ... [--configs cfg5_3d_512,cfg4_3d_256,grid:2048x2048] [--reps 20]
+                            [--rounds 2]
 
 Each library is loaded in its own subprocess; per config prints forward / inverse ms (CUDA events, mean
 of `reps` after 3 warm-ups), libraries interleaved `rounds` times to expose box drift.
@@ -29,7 +30,11 @@ def child(lib, configs, reps, k0=None):
     L.jt_destroy.argtypes = [P]
     out = {}
     for name in configs:
-        c = si.CONFIGS[name]
+        if name.startswith("grid:"):  # ad hoc grid "grid:2048x2048": (a, b) = (0.25, -0.25) per axis, eps 1e-12
+            shp = tuple(int(v) for v in name[5:].split("x"))
+            c = {"n": shp, "a": (0.25,) * len(shp), "b": (-0.25,) * len(shp), "eps": 1e-12}
+        else:
+            c = si.CONFIGS[name]
         d = len(c["n"])
         n = (ctypes.c_int64 * d)(*c["n"])
         a = (ctypes.c_double * d)(*c["a"])
