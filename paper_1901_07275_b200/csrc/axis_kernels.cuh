@@ -67,6 +67,15 @@ struct TermSplit {
 };
 
 // unroll factor of the batch-start W V loops (N > 512: all k0 degrees there, rows read through L1)
+// N > 1024 (factors through L1): issue a term's factor loads before the TMEM state reads they combine with
+// (bit 0: forward A1, bit 1: inverse bin sums at N >= JT_LF_INV_NMIN; measured: inverse 4096 -7 %, inverse
+// 2048 +1 %, forward 4096 +-0, forward 2048 +3 %)
+#ifndef JT_LF_INV_NMIN
+#define JT_LF_INV_NMIN 4096
+#endif
+#ifndef JT_LOADS_FIRST
+#define JT_LOADS_FIRST 2
+#endif
 #ifndef JT_VUNROLL
 #define JT_VUNROLL 4  // (the loads of 4 degrees in flight: N = 4096 forward -7 %, N = 2048 inverse -7 %)
 #endif
@@ -196,11 +205,23 @@ struct Cfg {
   // factor ring: stage = v_l (N complex) + u~_l (MAXR x NBINS complex) [+ chunk l of W V (VST): KPT degrees,
   // layout [m][c][kk], so the dense low-degree block is applied inside the term loop from SMEM]
   static constexpr bool STAGED = N <= 1024;
+  // N > 1024 forward: u~_l (the epilogue's factor, 32-64 KB) through a one-stage TMA ring in the SMEM left
+  // next to the exchange buffers (URING), filled a whole term ahead of its use; v_l still through L1
+// (measured: N = 2048 forward -5 %; N = 4096 +8 %: its 64 KB stage leaves too little L1 for the v_l loads)
+#ifndef JT_URING
+#define JT_URING 1
+#endif
+#ifndef JT_URING_NMAX
+#define JT_URING_NMAX 2048
+#endif
+  static constexpr bool URING_WANT = !STAGED && !INV && JT_URING && N <= JT_URING_NMAX;
   static constexpr bool VST = N <= 512;
   static constexpr int VUN = VST ? 1 : JT_VUNROLL;  // unroll of the batch-start W V loops
   static constexpr int KPT = VST ? VST_KPT : 0;
   static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
-  static constexpr int STAGE_BYTES = STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : 0;
+  static constexpr int SV_BYTES = STAGED ? V_BYTES : 0;  // v_l bytes in a ring stage (URING stages hold u~_l only)
+  static constexpr int STAGE_BYTES =
+      STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : (URING_WANT ? (U_BYTES + 127) / 128 * 128 : 0);
   // twiddle tables of the passes after the first, copied to SMEM (TWS): every twiddle is one broadcast
   // LDS.128 instead of a chain of complex multiplies
   static constexpr bool TWS = N <= 1024;
@@ -245,9 +266,10 @@ struct Cfg {
                ? gpc_fit(g - 1, nstage)
                : g;
   }
-  static constexpr int GPC = gpc_fit(8, 2);  // groups per CTA (one CTA per SM)
+  static constexpr int GPC = gpc_fit(8, STAGED ? 2 : 1);  // groups per CTA (one CTA per SM)
+  static constexpr bool URING = URING_WANT && GPC * GROUP_BYTES + hdr_bytes(1) <= SMEM_LIMIT;
   // a third ring stage when it fits next to the GPC groups
-  static constexpr int NSTAGE = (STAGED && GPC * GROUP_BYTES + hdr_bytes(3) <= SMEM_LIMIT) ? 3 : 2;
+  static constexpr int NSTAGE = (STAGED && GPC * GROUP_BYTES + hdr_bytes(3) <= SMEM_LIMIT) ? 3 : (URING ? 1 : 2);
   static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES + 3 * NSTAGE * 8;  // stages + full/empty barriers + counters
   static constexpr int BINFO_OFF = (RING_BYTES + 127) / 128 * 128;
   static constexpr int TW_OFF = BINFO_OFF + BINFO_BYTES;
@@ -340,18 +362,18 @@ struct Ring {
     return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES);
   }
   __device__ __forceinline__ double2 *u(long long seq) const {
-    return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::V_BYTES);
+    return reinterpret_cast<double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::SV_BYTES);
   }
   __device__ __forceinline__ const double *ph(long long seq) const {
-    return reinterpret_cast<const double *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::V_BYTES + C::U_BYTES);
+    return reinterpret_cast<const double *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::SV_BYTES + C::U_BYTES);
   }
   __device__ __forceinline__ void issue(long long seq) const {  // producer: one thread
     const int s = (int)(seq % C::NSTAGE);
     const int l = l0 + (int)(seq % rs);
     const bool kc = C::VST && l * C::KPT < k0;  // chunk l of W V exists (zero-padded to KPT degrees)
     const uint32_t ph_bytes = kc ? C::PH_BYTES : 0;
-    mbar_arrive_expect_tx(&full[s], C::V_BYTES + C::U_BYTES + ph_bytes);
-    tma_load_1d(v(seq), gv + (long long)l * C::N, C::V_BYTES, &full[s]);
+    mbar_arrive_expect_tx(&full[s], C::SV_BYTES + C::U_BYTES + ph_bytes);
+    if constexpr (C::STAGED) tma_load_1d(v(seq), gv + (long long)l * C::N, C::V_BYTES, &full[s]);
     tma_load_1d(u(seq), gu + (long long)l * C::MAXR * C::NBINS, C::U_BYTES, &full[s]);
     if (kc)
       tma_load_1d(const_cast<double *>(ph(seq)), gph + (long long)l * C::KPT * C::MAXR * C::NBINS, ph_bytes, &full[s]);
@@ -689,7 +711,7 @@ struct Ctx {
       double2 *t = reinterpret_cast<double2 *>(smem_raw + C::TW_OFF);
       for (int i = threadIdx.x; i < TwTotal<C::N, C::R>::value; i += C::NT) t[i] = __ldg(&tw[i]);
     }
-    if constexpr (C::STAGED) {
+    if constexpr (C::STAGED || C::URING) {
       if (threadIdx.x == 0) {
         for (int s = 0; s < C::NSTAGE; ++s) {
           mbar_init(&ring.full[s], 1);
@@ -749,14 +771,17 @@ struct Ctx {
     else return gv + (long long)l * C::N;
   }
   __device__ __forceinline__ const double2 *ufac(long long seq, int l) const {
-    if constexpr (C::STAGED) return ring.u(seq);
+    if constexpr (C::STAGED || C::URING) return ring.u(seq);
     else return gu + (long long)l * C::MAXR * C::NBINS;
   }
   __device__ __forceinline__ void acquire(long long seq) const {
     if constexpr (C::STAGED) ring.wait_full(seq);
   }
+  __device__ __forceinline__ void acquire_u(long long seq) const {  // URING: u~_l just before the epilogue
+    if constexpr (C::URING) ring.wait_full(seq);
+  }
   __device__ __forceinline__ void release(long long seq) const {
-    if constexpr (C::STAGED) ring.release(seq, gt);
+    if constexpr (C::STAGED || C::URING) ring.release(seq, gt);
   }
 };
 
@@ -788,6 +813,12 @@ struct State {
 #pragma unroll
       for (int i = 0; i < S; ++i) sm[i * C::GT + gt] = v[i];
     }
+  }
+  // TMEM state only: chunk c's loads issued, the caller waits (tmem_wait_ld) before reading o
+  __device__ __forceinline__ void chunk_issue(int c, double (&o)[CH]) const {
+    static_assert(C::TPRIV, "chunk_issue reads the TMEM state");
+    tmem_ld_d8(taddr + 32 * c, &o[0]);
+    tmem_ld_d8(taddr + 32 * c + 16, &o[8]);
   }
   __device__ __forceinline__ void chunk(int c, double (&o)[CH]) const {
     if constexpr (!C::PRIV) {
@@ -925,21 +956,49 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
         }
       }
       double xr[R], xi[R];
+      if constexpr (!C::STAGED && C::TPRIV && (JT_LOADS_FIRST & 1)) {
+        // A1, v_l from L1/L2: a chunk's loads issued between its TMEM state load and the wait for it
 #pragma unroll
-      for (int ch = 0; ch < State<C, R>::NCH; ++ch) {  // A1
-        double ac[State<C, R>::CH];
-        a.chunk(ch, ac);
+        for (int ch = 0; ch < State<C, R>::NCH; ++ch) {
+          double ac[State<C, R>::CH];
+          a.chunk_issue(ch, ac);
 #pragma unroll
-        for (int i = 0; i < State<C, R>::CH; ++i) {
-          const int r = ch * State<C, R>::CH + i;
-          if (r < R) {
-            const double2 vv = vl[vt + r * TPL];
-            xr[r] = vv.x * ac[i];
-            xi[r] = vv.y * ac[i];
+          for (int i = 0; i < State<C, R>::CH; ++i) {
+            const int r = ch * State<C, R>::CH + i;
+            if (r < R) {
+              const double2 vv = vl[vt + r * TPL];
+              xr[r] = vv.x;
+              xi[r] = vv.y;
+            }
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < State<C, R>::CH; ++i) {
+            const int r = ch * State<C, R>::CH + i;
+            if (r < R) {
+              xr[r] *= ac[i];
+              xi[r] *= ac[i];
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int ch = 0; ch < State<C, R>::NCH; ++ch) {  // A1
+          double ac[State<C, R>::CH];
+          a.chunk(ch, ac);
+#pragma unroll
+          for (int i = 0; i < State<C, R>::CH; ++i) {
+            const int r = ch * State<C, R>::CH + i;
+            if (r < R) {
+              const double2 vv = vl[vt + r * TPL];
+              xr[r] = vv.x * ac[i];
+              xi[r] = vv.y * ac[i];
+            }
           }
         }
       }
       fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // A2
+      cx.acquire_u(seq);
 #pragma unroll
       for (int q = 0; q < NB; ++q) {  // A3
         const int e = fwd_reg_of_bin<C>(q);
@@ -1075,6 +1134,30 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       // bin sums over the rows of the input bins q <= R/2 (positions > N/2 hold no rows), state read in chunks
       using YS = State<C, NB * MAXR>;
+      if constexpr (!C::STAGED && !C::VST && MAXR == 2 && (JT_LOADS_FIRST & 2) && C::N >= JT_LF_INV_NMIN) {
+        // u~_l from L1/L2: both rows' loads of every bin in flight before the state chunks
+        double2 u1[NB];
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+          const double2 u0 = ul[m[r]];
+          u1[r] = ul[NBINS + m[r]];
+          xr[r] = u0.x;
+          xi[r] = u0.y;
+        }
+#pragma unroll
+        for (int ch = 0; ch < YS::NCH; ++ch) {
+          double yc[YS::CH];
+          yb.chunk(ch, yc);
+#pragma unroll
+          for (int i = 1; i < YS::CH; i += 2) {
+            const int r = (ch * YS::CH + i) / 2;
+            if (r < NB) {
+              xr[r] = fma(u1[r].x, yc[i], xr[r] * yc[i - 1]);
+              xi[r] = fma(u1[r].y, yc[i], xi[r] * yc[i - 1]);
+            }
+          }
+        }
+      } else
 #pragma unroll
       for (int ch = 0; ch < YS::NCH; ++ch) {
         double yc[YS::CH];
