@@ -171,7 +171,7 @@ def config_block(args, cfg, ranks, k0s=None):
     return {"workload": f"{args.config}: {'x'.join(map(str, cfg['n']))} {kindtxt} forward, (a,b)="
                         f"{list(zip(cfg['a'], cfg['b']))}, eps={cfg['eps']}",
             "model": "none (transform)", "global_batch": 1, "seq_len": int(np.prod(cfg["n"])),
-            "ranks_per_axis": ranks, "k0_per_axis": k0s, "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
+            "ranks_per_axis": ranks, "k0_per_axis": k0s, "parallelism": f"slab{args.gpus}" if (args.gpus > 1 or args.slab) else "single",
             "l2_policy": "inputs (8 B x prod(n)) larger than the 126 MB L2; no extra flush"}
 
 
