@@ -76,13 +76,16 @@ struct TermSplit {
 #ifndef JT_LOADS_FIRST
 #define JT_LOADS_FIRST 2
 #endif
-// next-line L2 prefetch (measured: 256^3 forward -3.4 %; 512^3 forward +2.9 %, inverses +1..9 %: on only for the
-// forward with N <= JT_PREFETCH_NMAX)
+// next-line L2 prefetch (measured: 256^3 forward -3.4 %; 512^3 forward +2.9 %, 64^3 forward +8 %, inverses +1..9 %:
+// on only for the forward with N = 256)
 #ifndef JT_PREFETCH
 #define JT_PREFETCH 1
 #endif
 #ifndef JT_PREFETCH_NMAX
 #define JT_PREFETCH_NMAX 256
+#endif
+#ifndef JT_PREFETCH_NMIN
+#define JT_PREFETCH_NMIN 256
 #endif
 #ifndef JT_VUNROLL
 #define JT_VUNROLL 4  // (the loads of 4 degrees in flight: N = 4096 forward -7 %, N = 2048 inverse -7 %)
@@ -151,13 +154,18 @@ struct TwPrefix<N, R, NS, N> {
   static constexpr int value = 0;
 };
 
-template <int N_, int R_, int MAXR_, bool INV_>
+template <int N_, int R_, int MAXR_, bool INV_, bool WG_ = false>
 struct Cfg {
   static constexpr int N = N_, R = R_, MAXR = MAXR_;
   static constexpr bool INV = INV_;
+  // WG: one warp per group (LG = 32 / TPL lines) -- only for the term-split launches of few lines, which are
+  // latency-bound (no named barriers: 256^2 0.041 -> 0.033 ms); the large launches keep 4 lines per group,
+  // whose factor loads serve twice the lines per wavefront (one-warp groups measured +15 % at 512^3)
+  static constexpr bool WG = WG_;
   static constexpr int TPL = N / R;                                     // threads per line
   // lines per group (2 lines at TPL = 128 was measured 6 % slower at N = 4096: one 8-warp barrier domain)
-  static constexpr int LG = TPL <= 8 ? 32 / TPL : (TPL <= 32 ? 4 : 1);
+  // (WG applies to TPL = 16 only: at TPL = 32 one-line warps measured slower, 1024 x 64 inverse +7 %)
+  static constexpr int LG = TPL <= 8 ? 32 / TPL : (TPL <= 32 ? (WG && TPL == 16 ? 2 : 4) : 1);
   static constexpr int GT = TPL * LG;                                   // threads per group
   static constexpr int GW = GT / 32;                                    // warps per group
   static constexpr int NSL = LastNS<N, R>::value;                       // the last pass starts at sub-size NSL
@@ -886,7 +894,7 @@ struct LineAddr {
 template <class C, bool SPLIT>
 __device__ __forceinline__ void prefetch_next_line(const double *in, const Layout &lay, long long L, long long nlines,
                                                    int vt, int n) {
-  if constexpr (JT_PREFETCH && !C::INV && C::N <= JT_PREFETCH_NMAX) {
+  if constexpr (JT_PREFETCH && !C::INV && C::N <= JT_PREFETCH_NMAX && C::N >= JT_PREFETCH_NMIN) {
     if (L >= nlines) return;
     const bool mine = lay.inner == 1 ? (vt % 16 == 0) : (lay.inner % 16 == 0 ? (L % 16 == 0) : true);
     if (!mine) return;

@@ -192,7 +192,18 @@ jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
     }
   }
   const unsigned grid = ts.S > 1 ? (unsigned)(batches * ts.S) : (unsigned)std::min<long long>(batches, sms);
-  if constexpr (C::INV) {
+  if constexpr (C::WG) {  // (only reached for term-split launches: see launch_nmd)
+    if (ts.S <= 1) return fail(JT_ERR_ARG, "internal: one-warp-group configuration without term split");
+    if constexpr (C::INV) {
+      JT_CUDA_TRY(cudaFuncSetAttribute(jtk::inv_axis_kernel<C, false, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      jtk::inv_axis_kernel<C, false, true><<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
+    } else {
+      JT_CUDA_TRY(cudaFuncSetAttribute(jtk::fwd_axis_kernel<C, false, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      jtk::fwd_axis_kernel<C, false, true><<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
+    }
+  } else if constexpr (C::INV) {
     auto kern = ts.S > 1 ? jtk::inv_axis_kernel<C, false, true>
                          : (split ? jtk::inv_axis_kernel<C, true> : jtk::inv_axis_kernel<C, false>);
     JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -214,12 +225,34 @@ jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
   return JT_OK;
 }
 
+// Would launch_cfg<C> split the rank terms (few lines)?  Same test as inside launch_cfg.
+template <class C>
+bool term_split_applies(const jtk::AxisDev &ax, long long nlines, const jtk::Layout &lay, bool allow_ts, int sms) {
+  const long long batches = (nlines + (long long)C::GPC * C::LG - 1) / ((long long)C::GPC * C::LG);
+  const bool split = lay.in_cs != ax.n || lay.out_cs != ax.n;
+  return allow_ts && !split && nlines == lay.outer * lay.inner && ax.r >= 2 && batches > 0 && batches * 2 <= sms &&
+         std::min<long long>(ax.r, sms / batches) > 1;
+}
+
+template <int N, int MAXR, bool INV>
+jt_status launch_nmd(const jt_plan_s *p, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
+                     const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
+  using C = jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, INV>;
+  using CW = jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, INV, true>;
+  if constexpr (CW::LG != C::LG) {  // term-split launches with one-warp groups (Cfg::WG)
+    int dev = 0, sms = 148;
+    JT_CUDA_TRY(cudaGetDevice(&dev));
+    JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (term_split_applies<CW>(ax, nlines, lay, allow_ts, sms)) return launch_cfg<CW>(p, ax, in, out, nlines, lay, s, true);
+  }
+  return launch_cfg<C>(p, ax, in, out, nlines, lay, s, allow_ts);
+}
+
 template <int N, int MAXR>
 jt_status launch_nm(const jt_plan_s *p, bool inverse, const jtk::AxisDev &ax, const double *in, double *out,
                     long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
-  if (inverse)
-    return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, true>>(p, ax, in, out, nlines, lay, s, allow_ts);
-  return launch_cfg<jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, false>>(p, ax, in, out, nlines, lay, s, allow_ts);
+  if (inverse) return launch_nmd<N, MAXR, true>(p, ax, in, out, nlines, lay, s, allow_ts);
+  return launch_nmd<N, MAXR, false>(p, ax, in, out, nlines, lay, s, allow_ts);
 }
 
 template <int N>
