@@ -15,6 +15,12 @@
 #include "axis_kernels.cuh"
 #include "jt_internal.h"
 
+// staging slots of the *_host entry points: consecutive calls rotate through them, so a call's input copy only
+// waits for the output copy of the call JT_HOST_SLOTS back
+#ifndef JT_HOST_SLOTS
+#define JT_HOST_SLOTS 2
+#endif
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -106,10 +112,10 @@ struct jt_plan_s {
   int64_t total = 0;
   // *_host entry points: two staging slots (consecutive calls alternate, so one call's input copy overlaps the
   // previous call's output copy), their copy streams and events
-  double *stage_in[2] = {nullptr, nullptr}, *stage_out[2] = {nullptr, nullptr};
+  double *stage_in[JT_HOST_SLOTS] = {}, *stage_out[JT_HOST_SLOTS] = {};
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev[2 * 16 + 2] = {};
-  cudaEvent_t ev_free[2] = {nullptr, nullptr};  // slot's last output copy done
+  cudaEvent_t ev_free[JT_HOST_SLOTS] = {};  // slot's last output copy done
   unsigned host_calls = 0;
   // slab-distributed plans (jt_plan_dist): this rank's x-slab (forward input) / y-slab
   // (forward output) of the global n[0] x n[1] (x n[2]) array, the all-to-all buffers and the NCCL comm
@@ -312,7 +318,7 @@ void free_device(jt_plan_s *p) {
     cudaFree(p->dev[i].bstart);
     p->dev[i] = AxisDevBuf();
   }
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < JT_HOST_SLOTS; ++k) {
     cudaFree(p->stage_in[k]);
     cudaFree(p->stage_out[k]);
     p->stage_in[k] = p->stage_out[k] = nullptr;
@@ -551,7 +557,7 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     for (auto &e : p->ev) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : p->ev_free) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  const int slot = (int)(p->host_calls++ & 1u);
+  const int slot = (int)(p->host_calls++ % JT_HOST_SLOTS);
   if (!p->stage_in[slot]) {
     if (cudaMalloc((void **)&p->stage_in[slot], bytes) != cudaSuccess ||
         cudaMalloc((void **)&p->stage_out[slot], bytes) != cudaSuccess)
