@@ -223,16 +223,20 @@ def main():
         for ax in range(d - 1, -1, -1):
             strides.append((ax, int(np.prod(shape[:ax])), int(np.prod(shape[ax + 1:]))))
 
-        def step(evs=None):
+        def step(evs=None, count=None):
             src = x
             for i, (ax, outer, inner) in enumerate(strides):
                 if evs is not None:
                     evs[i].record(stream)
                 jt.jt_forward_axis(plan.handle, ax, src, y, outer, inner, stream)
+                if count is not None:  # kernels this axis call enqueued (the pass, + a reduction if term-split)
+                    count[0] += jt.jt_last_launches(plan.handle)
                 src = y
             if evs is not None:
                 evs[-1].record(stream)
-        launches_per_step = d
+        cnt = [0]
+        step(count=cnt)  # (an extra warm-up step) counts the library's kernel launches per step
+        launches_per_step = cnt[0]
         local_points = int(np.prod(shape))
     else:
         t_fac = time.perf_counter()
@@ -242,7 +246,8 @@ def main():
         k0s = [inf["k0"] for inf in plan.infos]
         x = plan.local_input(torch.from_numpy(si.gaussian(shape, seed=0)))
         step = plan.make_forward_step(x)
-        launches_per_step = plan.launches_per_step
+        step()  # (an extra warm-up step) counts the library's kernel launches per step
+        launches_per_step = jt.jt_last_launches(plan.handle)
         local_points = x.numel()
 
     for _ in range(args.warmup):

@@ -200,6 +200,12 @@ jt_status jt_plan_factors(jt_plan_t p, int axis, double *u_host, double *v_host,
  * rank cap used. */
 jt_status jt_plan_sigma(jt_plan_t p, int axis, double *sigma, int *count, int *rmax_used);
 
+/* Number of kernels the most recent transform call on p enqueued (jt_forward / jt_inverse / jt_adjoint, the
+ * *_host variants, jt_forward_axis / jt_inverse_axis / jt_axis_pass*): one fused axis pass per axis, plus one
+ * partial-sum reduction per axis whose rank terms were split over CTAs (few lines).  Used by bench.py's
+ * gpu_launches.  JT_ERR_ARG for a NULL p or count. */
+jt_status jt_last_launches(jt_plan_t p, int *count);
+
 /* Thread-local text of the last non-OK status ("" if none). */
 const char *jt_last_error(void);
 

@@ -35,7 +35,7 @@ EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_k
             "jt_plan_dist", "jt_local_box", "jt_forward_host_async", "jt_inverse_host_async", "jt_host_wait",
             "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
             "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_axis_pass_ex", "jt_destroy", "jt_plan_rank", "jt_plan_info",
-            "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_error", "jt_version",
+            "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_launches", "jt_last_error", "jt_version",
             "jt_debug_modified_pq"]
 
 
@@ -81,6 +81,7 @@ _lib.jt_plan_nodes.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_
 _lib.jt_plan_factors.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 _lib.jt_plan_sigma.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
                                ctypes.POINTER(ctypes.c_int)]
+_lib.jt_last_launches.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
 _lib.jt_last_error.restype = ctypes.c_char_p
 _lib.jt_version.restype = ctypes.c_char_p
 _lib.jt_debug_modified_pq.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p,
@@ -113,6 +114,13 @@ def _stream_handle(stream) -> int:
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def jt_last_launches(plan) -> int:
+    """Kernels the most recent transform call on `plan` (a Plan or a raw handle) enqueued."""
+    c = ctypes.c_int(0)
+    _check(_lib.jt_last_launches(getattr(plan, "handle", plan), ctypes.byref(c)), "jt_last_launches")
+    return c.value
 
 
 def jt_version() -> str:

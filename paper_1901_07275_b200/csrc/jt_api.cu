@@ -117,6 +117,7 @@ struct jt_plan_s {
   cudaEvent_t ev[2 * 16 + 2] = {};
   cudaEvent_t ev_free[JT_HOST_SLOTS] = {};  // slot's last output copy done
   unsigned host_calls = 0;
+  mutable int launches = 0;  // kernels enqueued by the latest transform call (jt_last_launches)
   // slab-distributed plans (jt_plan_dist): this rank's x-slab (forward input) / y-slab
   // (forward output) of the global n[0] x n[1] (x n[2]) array, the all-to-all buffers and the NCCL comm
   // term-split workspace (few-line launches, jtk::TermSplit)
@@ -221,7 +222,9 @@ jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
     kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
   }
   JT_CUDA_TRY(cudaGetLastError());
+  ++p->launches;
   if (ts.S > 1) {
+    ++p->launches;
     const long long total = nlines * ax.n;
     const int thr = 256;
     const unsigned g = (unsigned)std::min<long long>((total + thr - 1) / thr, 4LL * sms);
@@ -512,6 +515,7 @@ jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, dou
 // Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
 jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   jt_status st = check_device_plan(p);
+  p->launches = 0;
   if (st != JT_OK) return st;
   if (!in || !out) return fail(JT_ERR_ARG, "null data pointer");
   if (overlaps_partially(in, out, p->total)) return fail(JT_ERR_ARG, "input and output partially overlap");
@@ -547,6 +551,7 @@ jt_status host_wait(jt_plan_s *p) {
 jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double *out_h, cudaStream_t s,
                          bool wait) {
   jt_status st = check_device_plan(p);
+  p->launches = 0;
   if (st != JT_OK) return st;
   if (!in_h || !out_h) return fail(JT_ERR_ARG, "null host pointer");
   DeviceGuard g(p->device);
@@ -623,6 +628,12 @@ extern "C" {
 const char *jt_last_error(void) { return g_last_error.c_str(); }
 
 const char *jt_version(void) { return "jt 0.1 (sm_100a fused fp64 axis passes)"; }
+
+jt_status jt_last_launches(jt_plan_t p, int *count) {
+  if (!p || !count) return fail(JT_ERR_ARG, "null argument");
+  *count = p->launches;
+  return JT_OK;
+}
 
 jt_status jt_default_opts(jt_opts *o) {
   if (!o) return fail(JT_ERR_ARG, "null opts");
@@ -789,6 +800,7 @@ jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs
 static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *in, double *out, int64_t outer,
                             int64_t inner, int in_split, int out_split, void *stream, int64_t ostride = -1) {
   jt_status st = check_device_plan(p);
+  if (p) p->launches = 0;
   if (st != JT_OK) return st;
   if (axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad axis");
   if (!in || !out || outer < 0 || inner < 1) return fail(JT_ERR_ARG, "bad pointers / shape");

@@ -68,7 +68,6 @@ class SlabPlan:
         self._axis = axis_pass
         self._send = torch.empty(self.count, dtype=torch.float64, device=self.device)
         self._recv = torch.empty(self.count, dtype=torch.float64, device=self.device)
-        self.launches_per_step = self.d  # axis passes (the all-to-all is NCCL's)
 
     # ---- geometry ----
     def local_box(self, which: int):
@@ -253,7 +252,6 @@ class LibSlabPlan:
         self.x_shape = tuple(h - l for l, h in zip(lo0, hi0))
         self.y_shape = tuple(h - l for l, h in zip(lo1, hi1))
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self.launches_per_step = self.d  # axis passes (the all-to-all is NCCL's)
 
     def local_box(self, which: int):
         return self.box[which]

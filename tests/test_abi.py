@@ -68,6 +68,13 @@ def test_destroy_null_ok():
     assert jt._lib.jt_destroy(None) == jt.JT_OK
 
 
+def test_last_launches_arguments():
+    assert jt._lib.jt_last_launches(None, None) == jt.JT_ERR_ARG
+    p = jt.Plan(64, 0.1, -0.2, device=-2)
+    assert jt.jt_last_launches(p) == 0  # no transform yet
+    p.close()
+
+
 def test_debug_hook_errors():
     with pytest.raises(jt.JTError):
         jt.jt_debug_modified_pq(1.5, 0.0, [1.0], 3)

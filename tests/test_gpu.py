@@ -344,3 +344,22 @@ def test_term_split_launches(shape, a, b):
     x = si.gaussian(shape, seed=23)
     assert relerr(gpu_forward(p, x), oracle.forward(x, a, b)) <= TOL
     assert relerr(gpu_forward(p, x, inverse=True), oracle.inverse(x, a, b)) <= TOL
+
+
+def test_last_launches_counts_kernels():
+    """jt_last_launches (bench.py's gpu_launches): one fused pass per axis, plus one reduction per term-split axis."""
+    p = jt.Plan((128, 128, 128), 0.2, -0.3, 1e-12)  # 16384 lines per axis: no term split
+    x = torch.from_numpy(si.gaussian((128, 128, 128), seed=3)).cuda()
+    y = torch.empty_like(x)
+    jt.jt_forward(p.handle, x, y)
+    assert jt.jt_last_launches(p) == 3
+    jt.jt_forward_axis(p.handle, 1, x, y, 128, 128)
+    assert jt.jt_last_launches(p) == 1
+    p.close()
+    q = jt.Plan(1024, 0.25, -0.3, 1e-12)  # one line: term split + ts_reduce
+    x1 = torch.from_numpy(si.gaussian((1024,), seed=3)).cuda()
+    y1 = torch.empty_like(x1)
+    jt.jt_inverse(q.handle, x1, y1)
+    assert jt.jt_last_launches(q) == 2
+    torch.cuda.synchronize()
+    q.close()
