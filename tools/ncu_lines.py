@@ -62,12 +62,14 @@ def line_map(lib, mangled_hint):
 def main(rep, kregex, lib, skip=0, top=40):
     kname, rows = sass_rows(rep, kregex, skip)
     # mangled-name hint: template args of Cfg<N, R, MAXR>
-    nums = re.findall(r"\(int\)(\d+)", kname)
-    bools = re.findall(r"\(bool\)(\d)", kname)  # Cfg's INV, then the kernel's SPLIT [, TSPLIT]
+    cfg = re.search(r"Cfg<([^>]*)>", kname)
+    nums = re.findall(r"\(int\)(\d+)", cfg.group(1))
+    cbools = re.findall(r"\(bool\)(\d)", cfg.group(1))                 # Cfg's INV [, WG]
+    kbools = re.findall(r"\(bool\)(\d)", kname[cfg.end():].split(">(")[0])  # the kernel's SPLIT, TSPLIT
     base = "fwd_axis_kernel" if "fwd_axis" in kname else "inv_axis_kernel"
     hint = base + r"INS_3CfgILi" + r"ELi".join(nums) + "E"
-    if bools:
-        hint += "Lb" + bools[0] + "EEE" + "".join("Lb" + b + "E" for b in bools[1:]) + "E"
+    if cbools:
+        hint += "".join("Lb" + b + "E" for b in cbools) + "EE" + "".join("Lb" + b + "E" for b in kbools) + "E"
     maps = line_map(lib, hint)
     if not maps:
         print("no line map for", hint)
