@@ -68,6 +68,11 @@ def _worker(rank, world, port, shape, a, b, q):
         yv = si.gaussian(shape, seed=4)
         ws = sp.inverse(sp.local_output(yv))
         e_inv = float(np.max(np.abs(ws.numpy() - oracle.inverse(yv, a, b)[lo0[0]:hi0[0]])))
+        # other pipeline depths (one chunk, a ragged split, one row per chunk) give the same slabs
+        R = shape[0] // world
+        for k in sorted({1, 3, R}):
+            e_fwd = max(e_fwd, float(np.max(np.abs(sp.forward(xs, chunks=k).numpy() - ys.numpy()))))
+            e_inv = max(e_inv, float(np.max(np.abs(sp.inverse(sp.local_output(yv), chunks=k).numpy() - ws.numpy()))))
         q.put((rank, e_fwd, e_rt, e_inv, tuple(ys.shape), tuple(ws.shape)))
     except Exception as ex:  # report instead of hanging the parent
         q.put((rank, repr(ex)))
