@@ -39,6 +39,7 @@
 
 #include "fft_regs.cuh"
 #include "tmem.cuh"
+#include "tuning.h"
 
 namespace jtk {
 
@@ -66,30 +67,7 @@ struct TermSplit {
   double *part;
 };
 
-// unroll factor of the batch-start W V loops (N > 512: all k0 degrees there, rows read through L1)
-// N > 1024 (factors through L1): issue a term's factor loads before the TMEM state reads they combine with
-// (bit 0: forward A1, bit 1: inverse bin sums at N >= JT_LF_INV_NMIN; measured: inverse 4096 -7 %, inverse
-// 2048 +1 %, forward 4096 +-0, forward 2048 +3 %)
-#ifndef JT_LF_INV_NMIN
-#define JT_LF_INV_NMIN 4096
-#endif
-#ifndef JT_LOADS_FIRST
-#define JT_LOADS_FIRST 2
-#endif
-// next-line L2 prefetch (measured: 256^3 forward -3.4 %; 512^3 forward +2.9 %, 64^3 forward +8 %, inverses +1..9 %:
-// on only for the forward with N = 256)
-#ifndef JT_PREFETCH
-#define JT_PREFETCH 1
-#endif
-#ifndef JT_PREFETCH_NMAX
-#define JT_PREFETCH_NMAX 256
-#endif
-#ifndef JT_PREFETCH_NMIN
-#define JT_PREFETCH_NMIN 256
-#endif
-#ifndef JT_VUNROLL
-#define JT_VUNROLL 4  // (the loads of 4 degrees in flight: N = 4096 forward -7 %, N = 2048 inverse -7 %)
-#endif
+// (build-time tuning knobs JT_*: tuning.h)
 
 constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
 constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
@@ -177,35 +155,14 @@ struct Cfg {
   // (the forward's bin rows y: 2 NB MAXR, or the inverse's acc: 2R).  For R >= 32 that exceeds 255, so
   // the input state lives in a thread-private SMEM area (PRIV), read once per term (8 B per point), and
   // the exchange runs one real plane at a time (SPLITX) to leave SMEM for the factor ring.
-#ifndef JT_PRIV16
-#define JT_PRIV16 1
-#endif
-#ifndef JT_REGS16
-#define JT_REGS16 168
-#endif
-#ifndef JT_REGS16F
-#define JT_REGS16F 128
-#endif
   static constexpr bool PRIV = R >= 32 || (JT_PRIV16 && N >= 64);
   // PRIV state in tensor memory (TPRIV, tcgen05.ld/st): frees the SMEM crossbar of the per-term state re-reads
-#ifndef JT_TPRIV
-#define JT_TPRIV 1
-#endif
-#ifndef JT_TPRIV_NMAX
-#define JT_TPRIV_NMAX 4096
-#endif
   static constexpr bool TPRIV = PRIV && JT_TPRIV && N <= JT_TPRIV_NMAX;
-#ifndef JT_SPLITX_TPRIV
-#define JT_SPLITX_TPRIV 0
-#endif
   // exchange one real plane at a time (3 group barriers per exchange) only while SMEM is short: with the state
   // in TMEM the full complex exchange (1 barrier) fits
   static constexpr bool SPLITX = R >= 32 && (!TPRIV || JT_SPLITX_TPRIV);
 
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
-#ifndef JT_REGS16M4
-#define JT_REGS16M4 168
-#endif
   // (MAXR = 4: twice the row accumulators / bin rows per thread)
   static constexpr int REGS = R >= 32 ? 255
                                       : (PRIV ? (MAXR > 2 ? JT_REGS16M4 : (INV ? JT_REGS16 : JT_REGS16F))
@@ -224,12 +181,6 @@ struct Cfg {
   // N > 1024 forward: u~_l (the epilogue's factor, 32-64 KB) through a one-stage TMA ring in the SMEM left
   // next to the exchange buffers (URING), filled a whole term ahead of its use; v_l still through L1
 // (measured: N = 2048 forward -5 %; N = 4096 +8 %: its 64 KB stage leaves too little L1 for the v_l loads)
-#ifndef JT_URING
-#define JT_URING 1
-#endif
-#ifndef JT_URING_NMAX
-#define JT_URING_NMAX 2048
-#endif
   static constexpr bool URING_WANT = !STAGED && !INV && JT_URING && N <= JT_URING_NMAX;
   static constexpr bool VST = N <= 512;
   static constexpr int VUN = VST ? 1 : JT_VUNROLL;  // unroll of the batch-start W V loops
@@ -242,27 +193,9 @@ struct Cfg {
   // LDS.128 instead of a chain of complex multiplies
   static constexpr bool TWS = N <= 1024;
   // ... and with the state in TMEM, each thread's own twiddles (constant for the kernel) in its TMEM slice (TWT)
-#ifndef JT_TWT
-#define JT_TWT 1
-#endif
   static constexpr int TWPT = TwPerThread<N, R>::value;  // complex twiddles per thread
   // (MAXR 4: slice too small; the R = 32 inverse measured 2 % slower with it)
-#ifndef JT_TWT_INV32
-#define JT_TWT_INV32 0
-#endif
-#ifndef JT_TWT_LARGE
-#define JT_TWT_LARGE 1
-#endif
 // twiddles per TMEM wait in the N > 1024 passes (measured: forward 4 -5 % vs 8 at N = 4096; inverse 8 -3 % at 2048)
-#ifndef JT_TWT_CH_LARGE_F
-#define JT_TWT_CH_LARGE_F 4
-#endif
-#ifndef JT_TWT_CH_LARGE_I
-#define JT_TWT_CH_LARGE_I 8
-#endif
-#ifndef JT_TWT_LARGE_INV_NMAX
-#define JT_TWT_LARGE_INV_NMAX 2048  // (the N = 4096 inverse measured 1 % slower with it, N = 2048 2 % faster)
-#endif
   // N > 1024 (no SMEM table, TWS off): the twiddles in TMEM too, one copy per lane quadrant shared by the warps
   // of that quadrant (TW_SHARED: warps w and w + 4 have the same thread positions vt when the group size
   // divides 128), after all the warps' state slices

@@ -15,11 +15,8 @@
 #include "axis_kernels.cuh"
 #include "jt_internal.h"
 
-// staging slots of the *_host entry points: consecutive calls rotate through them, so a call's input copy only
-// waits for the output copy of the call JT_HOST_SLOTS back
-#ifndef JT_HOST_SLOTS
-#define JT_HOST_SLOTS 2
-#endif
+// (JT_HOST_SLOTS, JT_R512, JT_R4096: tuning.h.)  The *_host entry points rotate through JT_HOST_SLOTS staging
+// slots, so a call's input copy only waits for the output copy of the call JT_HOST_SLOTS back.
 
 namespace {
 
@@ -154,12 +151,6 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
 // (16x16, 32x16, 32x32), two for 2048 and 4096 (32x32x2, 32x32x4); see DESIGN.md "Kernels".
 // MAXR = 4 (more than two nodes in some bin: only for (a, b) near the ends of (-1, 1)) always uses
 // radix 16, whose accumulators fit in registers.
-#ifndef JT_R512
-#define JT_R512 32
-#endif
-#ifndef JT_R4096
-#define JT_R4096 32
-#endif
 template <int N, int MAXR>
 constexpr int radix_for() {
   return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32)))));

@@ -1,0 +1,84 @@
+// Build-time tuning knobs of the axis-pass kernels and the C ABI.  Each default is the
+// measured winner of an A/B on one B200 (tools/ab_time.py); override with -DJT_...=v (build.py `defines`) to
+// repeat an experiment.  Nothing here changes results beyond rounding order.
+#pragma once
+
+// ---- register budgets and per-thread state ----------------------------------------------------------------
+#ifndef JT_PRIV16
+#define JT_PRIV16 1  // radix-16 kernels (N >= 64) keep their per-batch state out of registers (PRIV)
+#endif
+#ifndef JT_REGS16
+#define JT_REGS16 168  // registers of the radix-16 inverse kernels
+#endif
+#ifndef JT_REGS16F
+#define JT_REGS16F 128  // registers of the radix-16 forward kernels (16 warps/SM: 256^3-class forwards -4.8 %)
+#endif
+#ifndef JT_REGS16M4
+#define JT_REGS16M4 168  // MAXR = 4 radix-16 kernels (128 spilled: nonuniform 256^3 forward 3.85 -> 3.00 ms)
+#endif
+#ifndef JT_TPRIV
+#define JT_TPRIV 1  // per-batch state in tensor memory (tcgen05.ld/st) instead of SMEM
+#endif
+#ifndef JT_TPRIV_NMAX
+#define JT_TPRIV_NMAX 4096  // ... for FFT lengths up to this
+#endif
+#ifndef JT_SPLITX_TPRIV
+#define JT_SPLITX_TPRIV 0  // 1: exchange one real plane at a time even with the state in TMEM (3 barriers)
+#endif
+
+// ---- twiddles ----------------------------------------------------------------------------------------------
+#ifndef JT_TWT
+#define JT_TWT 1  // per-thread twiddles in TMEM (N <= 1024: 512^3 forward 17.9 -> 17.3 ms)
+#endif
+#ifndef JT_TWT_INV32
+#define JT_TWT_INV32 0  // ... also for the radix-32 inverse (measured 2 % slower)
+#endif
+#ifndef JT_TWT_LARGE
+#define JT_TWT_LARGE 1  // N > 1024: one TMEM twiddle copy per lane quadrant (4096^2 forward 4.05 -> 3.81 ms)
+#endif
+#ifndef JT_TWT_LARGE_INV_NMAX
+#define JT_TWT_LARGE_INV_NMAX 2048  // ... inverses up to this N (N = 4096 inverse 1 % slower, N = 2048 2 % faster)
+#endif
+#ifndef JT_TWT_CH_LARGE_F
+#define JT_TWT_CH_LARGE_F 4  // N > 1024 forward: twiddles per TMEM wait (4 vs 8: -5 % at N = 4096)
+#endif
+#ifndef JT_TWT_CH_LARGE_I
+#define JT_TWT_CH_LARGE_I 8  // N > 1024 inverse: twiddles per TMEM wait (8 vs 4: -3 % at N = 2048)
+#endif
+
+// ---- factor and input loads --------------------------------------------------------------------------------
+#ifndef JT_URING
+#define JT_URING 1  // N > 1024 forward: one-stage TMA ring for u~_l in spare SMEM
+#endif
+#ifndef JT_URING_NMAX
+#define JT_URING_NMAX 2048  // ... up to this N (2048 forward -5 %; 4096 +8 %: the stage starves L1)
+#endif
+#ifndef JT_LOADS_FIRST
+#define JT_LOADS_FIRST 2  // bit 0: forward A1, bit 1: inverse bin sums issue factor loads before the TMEM state
+#endif
+#ifndef JT_LF_INV_NMIN
+#define JT_LF_INV_NMIN 4096  // ... bit 1 from this N (4096 inverse -7 %, 2048 +1 %; bit 0: 2048 forward +3 %)
+#endif
+#ifndef JT_VUNROLL
+#define JT_VUNROLL 4  // N > 512: batch-start W V loops unrolled (4096 forward -7 %, 2048 inverse -7 %)
+#endif
+#ifndef JT_PREFETCH
+#define JT_PREFETCH 1  // next-line L2 prefetch at batch start ...
+#endif
+#ifndef JT_PREFETCH_NMIN
+#define JT_PREFETCH_NMIN 256  // ... for forwards with N in [NMIN, NMAX] (256^3 -3.4 %; 64^3 +8 %, 512^3 +2.9 %)
+#endif
+#ifndef JT_PREFETCH_NMAX
+#define JT_PREFETCH_NMAX 256
+#endif
+
+// ---- radix and host pipeline (jt_api.cu) -------------------------------------------------------------------
+#ifndef JT_R512
+#define JT_R512 32  // register radix at N = 512 (16: two exchanges, 26.4 vs 21.7 ms at 512^3)
+#endif
+#ifndef JT_R4096
+#define JT_R4096 32  // register radix at N = 4096
+#endif
+#ifndef JT_HOST_SLOTS
+#define JT_HOST_SLOTS 2  // staging slots of the *_host entry points (3: no change in the 512^3 e2e stream)
+#endif
