@@ -30,10 +30,14 @@ eps 1.08e-19), rounded once to float64; the separable apply runs in float64
 with numpy's BLAS (a library matmul serves as the mode-product step).  The
 literal O(n^{2d}) Kronecker sum is `kron_matrix` (small sizes only).
 
-Every function here is pinned by `tests/test_oracle.py` against things other
-than itself (DCT-II/III and DST-I closed forms via scipy, gamma-function endpoint
-values, Beta-function moments via mpmath, 40-digit mpmath Golub-Welsch +
-hypergeometric Jacobi values, orthogonality).  No function is "parity unpinned".
+Every function here is pinned by `tests/test_oracle.py` and (the NEXT-row functions:
+phi_points, cauchy_h0 / modified_q_all, phi_q_uniform, forward_ex, adjoint_ex,
+forward_axes) `tests/test_next.py` against things other than itself (DCT-II/III,
+DST-I and DST-III closed forms via scipy, trigonometric closed forms summed
+literally, gamma-function endpoint values, Beta-function moments via mpmath,
+40-digit mpmath Golub-Welsch + hypergeometric Jacobi values, scipy Jacobi
+polynomials, mpmath Ferrers Q, the Wronskian, orthogonality and the adjoint
+identity).  No function is "parity unpinned".
 """
 from __future__ import annotations
 

@@ -198,3 +198,76 @@ def test_clustered_points_spread_over_bins():
     assert np.all(np.diff(bins) >= 0)
     assert np.bincount(bins).max() <= 4
     assert np.max(np.abs(bins - np.rint(t * N / (2 * np.pi)))) <= 2
+
+
+# ---------------------------------------------------------------------------------------------------
+# oracle pins: the composed nonuniform / second-kind transforms (forward_ex, adjoint_ex, forward_axes)
+# ---------------------------------------------------------------------------------------------------
+def _cheb_matrix(t, n, kind):
+    """a = b = -1/2 closed forms: P~_k(t) = sqrt(2/pi) cos(k t) (k >= 1), 1/sqrt(pi) (k = 0); Q~_k(t) =
+    sqrt(2/pi) sin(k t) (pinned above against the oracle's own P~ / Q~ generators)."""
+    k = np.arange(n)
+    if kind == 0:
+        M = np.sqrt(2 / np.pi) * np.cos(np.outer(t, k))
+        M[:, 0] = 1 / np.sqrt(np.pi)
+    else:
+        M = np.sqrt(2 / np.pi) * np.sin(np.outer(t, k))
+    return M
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_forward_ex_literal_double_sum(kind):
+    """forward_ex / adjoint_ex at random angles (PAPER.md:491, 634, 676: values f(t_i, s_j) = sum_{k,l}
+    J_k(t_i) J_l(s_j) alpha_{kl}) against the literal double sum of the closed-form entries."""
+    rng = np.random.default_rng(11)
+    n0, n1 = 7, 9
+    t0, t1 = np.sort(rng.uniform(0.01, np.pi - 0.01, n0)), np.sort(rng.uniform(0.01, np.pi - 0.01, n1))
+    A, B = _cheb_matrix(t0, n0, kind), _cheb_matrix(t1, n1, kind)
+    x = rng.standard_normal((n0, n1))
+    ref = np.zeros((n0, n1))
+    for i in range(n0):
+        for j in range(n1):
+            ref[i, j] = sum(A[i, k] * B[j, l] * x[k, l] for k in range(n0) for l in range(n1))
+    ab = (-0.5, -0.5)
+    np.testing.assert_allclose(oracle.forward_ex(x, ab, ab, [t0, t1], kind), ref, atol=1e-13)
+    refT = np.zeros((n0, n1))
+    for k in range(n0):
+        for l in range(n1):
+            refT[k, l] = sum(A[i, k] * B[j, l] * x[i, j] for i in range(n0) for j in range(n1))
+    np.testing.assert_allclose(oracle.adjoint_ex(x, ab, ab, [t0, t1], kind), refT, atol=1e-13)
+
+
+def test_forward_ex_second_kind_uniform_is_a_sine_transform():
+    """Uniform second kind at a = b = -1/2: nodes t_j = (2j+1) pi / (2n), w_j = pi / n, so the weighted matrix is
+    sqrt(2/n) sin(k t_j) -- for k = 1..n-1 the orthonormal DST-II basis (scipy DST-III of the shifted vector)."""
+    import scipy.fft as sfft
+    n = 12
+    x = np.random.default_rng(3).standard_normal(n)
+    x[0] = 0.0  # Q~_0 = 0: the k = 0 column is zero
+    got = oracle.forward_ex(x, (-0.5,), (-0.5,), None, 1)
+    # sum_{k=1}^{n-1} sqrt(2/n) sin(pi k (2j+1) / (2n)) x_k = DST-III (orthonormal) of (x_1, ..., x_{n-1}, 0)
+    y = np.append(x[1:], 0.0)
+    np.testing.assert_allclose(got, sfft.dst(y, type=3, norm="ortho"), atol=1e-13)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_adjoint_ex_is_the_transpose(kind):
+    """<forward_ex(x), y> = <x, adjoint_ex(y)> for general (a, b), 3D, mixed uniform / nonuniform axes."""
+    rng = np.random.default_rng(17)
+    shape = (6, 5, 7)
+    a, b = (0.3, -0.6, 0.1), (-0.2, 0.45, 0.7)
+    pts = [np.sort(rng.uniform(0.05, 3.0, 6)), None, np.sort(rng.uniform(0.05, 3.0, 7))]
+    x, y = rng.standard_normal(shape), rng.standard_normal(shape)
+    lhs = float(np.sum(oracle.forward_ex(x, a, b, pts, kind) * y))
+    rhs = float(np.sum(x * oracle.adjoint_ex(y, a, b, pts, kind)))
+    assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+
+
+def test_forward_axes_composes_to_the_full_transform():
+    """Axis passes in any order and grouping give the full transform (the operator is a Kronecker product)."""
+    rng = np.random.default_rng(19)
+    shape, a, b = (5, 6, 4), (0.2, -0.3, 0.5), (0.1, 0.4, -0.6)
+    x = rng.standard_normal(shape)
+    full = oracle.forward(x, a, b)
+    np.testing.assert_allclose(oracle.forward_axes(oracle.forward_axes(x, a, b, [2]), a, b, [0, 1]), full, atol=1e-14)
+    np.testing.assert_allclose(oracle.forward_axes(x, a, b, [1, 0, 2]), full, atol=1e-14)
