@@ -153,10 +153,10 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
 // radix 16, whose accumulators fit in registers.
 template <int N, int MAXR>
 constexpr int radix_for() {
-  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32)))));
+  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32))))));
 }
 int radix_of(int64_t N, int maxr) {
-  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N <= 256 ? 16 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32)))));
+  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32))))));
 }
 
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
