@@ -47,8 +47,22 @@ def both():
     cur.wait_stream(s2)
 
 
+def d2h_pitched():
+    # the e2e pipeline's D2H pattern (jt_api.cu transform_host): 8 column blocks of a (512, cols) row-major array,
+    # each one cudaMemcpy2DAsync (cuda-python; torch's strided host copies do not use it)
+    from cuda.bindings import runtime as rt
+    rows = 512
+    cols = (nbytes // 8) // rows
+    st = torch.cuda.current_stream().cuda_stream
+    for c in range(8):
+        c0, c1 = cols * c // 8, cols * (c + 1) // 8
+        off = c0 * 8
+        rt.cudaMemcpy2DAsync(h_out.data_ptr() + off, cols * 8, d_out.data_ptr() + off, cols * 8, (c1 - c0) * 8, rows,
+                             rt.cudaMemcpyKind.cudaMemcpyDeviceToHost, st)
+
+
 res = {"bytes": nbytes}
-for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both)):
+for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both), ("d2h_pitched", d2h_pitched)):
     ms = timed(fn)
     res[name + "_ms"] = ms
     res[name + "_GBps"] = (2 if name == "both" else 1) * nbytes / ms / 1e6
