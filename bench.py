@@ -119,6 +119,37 @@ def cpu_oracle_rate(cfg, max_seconds: float = 30.0):
     return float(np.prod(shape)) / dt, desc, threads
 
 
+def cpu_oracle_rate_one_core(cfg):
+    """The oracle on ONE core (the paper's single-processor setting), on a bounded
+    sample: axes d-1..1 on an x-slab of n0/32 planes (the whole 1D transform for d = 1).  Returns
+    (coefficients/s of the whole transform at that per-point cost, sample description) or None."""
+    import oracle
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        return None
+    shape, a, b = cfg["n"], cfg["a"], cfg["b"]
+    pts, kind = si.config_points(cfg), cfg.get("kind", 0)
+    x = si.gaussian(shape, seed=0)
+    d = len(shape)
+    for ax in range(d):  # the matrices (the oracle's "fac") are built outside the timed region
+        oracle.axis_matrix(shape[ax], a[ax], b[ax], None if pts is None else pts[ax], kind)
+    with threadpool_limits(limits=1):
+        if d == 1:
+            t0 = time.perf_counter()
+            oracle.forward_ex(x, a, b, pts, kind)
+            dt = time.perf_counter() - t0
+            return float(x.size) / dt, f"full 1D forward on one core, {dt * 1e3:.2f} ms"
+        slab = max(1, shape[0] // 32)
+        xs = np.ascontiguousarray(x[:slab])
+        t0 = time.perf_counter()
+        oracle.forward_axes(xs, a, b, axes=list(range(d - 1, 0, -1)), points=pts, kind=kind)
+        dt = time.perf_counter() - t0
+    return (xs.size * (d - 1) / dt / d,
+            f"one core: axes {d - 1}..1 on an x-slab of {slab} planes ({xs.size * (d - 1)} axis-pass points, "
+            f"{dt:.2f} s); value = axis-pass points/s / d")
+
+
 def run_reference(args, cfg, rank: int):
     """--impl reference: the CPU oracle timed on the host (rank 0 only)."""
     if rank != 0:
@@ -312,6 +343,9 @@ def main():
                     "flops_per_launch": flops,
                     "per_axis_ms_launch_order": [round(float(v), 4) for v in per_axis_ms],
                     "hbm_algorithmic_GBps": hbm_bytes / (per_axis_ms[i_dom] * 1e-3) / 1e9,
+                    # ncu-measured DRAM bytes of one launch (profiles/ncu_summary.json) over the live launch time
+                    "hbm_measured_frac": (traffic / (per_axis_ms[i_dom] * 1e-3) / 1e9 / load_peaks()["hbm_gbs"]
+                                          if traffic else None),
                     "hbm_frac_of_measured": hbm_bytes / (per_axis_ms[i_dom] * 1e-3) / 1e9 / load_peaks()["hbm_gbs"],
                     # SURVEY.md §8(d) "north-star model": the HBM traffic an unfused one-rank-term-per-pass schedule
                     # would move (24 B per point per term: read input, read + write the accumulator) over the
@@ -375,6 +409,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, desc, threads = cpu_oracle_rate(cfg)
         cpu = {"value": v, "unit": "coefficients/s", "cores": threads, "kind": "oracle", "sample": desc}
+        one = cpu_oracle_rate_one_core(cfg)
+        if one is not None:
+            cpu["one_core"] = {"value": one[0], "unit": "coefficients/s", "cores": 1, "sample": one[1]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "coefficients/s", "n_gpus": args.gpus, "steps": args.steps,
