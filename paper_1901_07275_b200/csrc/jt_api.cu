@@ -148,15 +148,15 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
 }
 
 // Radix of the first (register) pass for FFT length N: one SMEM exchange per term for N <= 1024
-// (16x16, 32x16, 32x32), two for 2048 and 4096 (32x32x2, 32x32x4); see DESIGN.md "Kernels".
+// (16x16, 32x16, 32x32), two for 2048 and 4096 (16x16x8, 32x32x4); see DESIGN.md "Kernels".
 // MAXR = 4 (more than two nodes in some bin: only for (a, b) near the ends of (-1, 1)) always uses
 // radix 16, whose accumulators fit in registers.
 template <int N, int MAXR>
 constexpr int radix_for() {
-  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32))))));
+  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : (N == 2048 ? JT_R2048 : 32)))))));
 }
 int radix_of(int64_t N, int maxr) {
-  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : 32))))));
+  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : (N == 2048 ? JT_R2048 : 32)))))));
 }
 
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
