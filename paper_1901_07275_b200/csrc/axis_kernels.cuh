@@ -57,6 +57,7 @@ struct AxisDev {
   const int *bstart;     // nbins + 1 row offsets: rows of bin m are bstart[m] .. bstart[m+1]-1
   const double2 *tw;     // per-pass twiddle tables, see TwOff (pass NS, radix RS: (RS-1) NS entries,
                          // entry (r-1) NS + j = e^{+2 pi i j r / (NS RS)})
+  const double2 *tw_ts;  // the same for the radix of the term-split launches where it differs (else == tw)
 };
 
 // Term split (few lines: latency-bound launches).  S > 1: CTA b handles batch b / S and only the rank terms

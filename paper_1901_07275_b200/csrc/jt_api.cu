@@ -34,7 +34,7 @@ jt_status fail(jt_status s, const std::string &msg) {
   } while (0)
 
 struct AxisDevBuf {
-  double2 *ub = nullptr, *v = nullptr, *tw = nullptr;
+  double2 *ub = nullptr, *v = nullptr, *tw = nullptr, *tw_ts = nullptr;  // tw_ts: only if the radixes differ
   double *phivb = nullptr, *phivc = nullptr;
   int *bstart = nullptr;
   int maxr = 0;  // row slots per bin in ub / phivb (template MAXR of the kernels)
@@ -144,6 +144,7 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
   ax.phivc = p->dev[axis].phivc;
   ax.bstart = p->dev[axis].bstart;
   ax.tw = p->dev[axis].tw;
+  ax.tw_ts = p->dev[axis].tw_ts ? p->dev[axis].tw_ts : p->dev[axis].tw;
   return ax;
 }
 
@@ -151,12 +152,23 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
 // (16x16, 32x16, 32x32), two for 2048 and 4096 (16x16x8, 32x32x4); see DESIGN.md "Kernels".
 // MAXR = 4 (more than two nodes in some bin: only for (a, b) near the ends of (-1, 1)) always uses
 // radix 16, whose accumulators fit in registers.
+constexpr int radix_of(int64_t N, int maxr) {
+  return maxr > 2    ? 16
+         : N == 16   ? 16
+         : N == 32   ? 32
+         : N == 64   ? JT_R64
+         : N == 128  ? JT_R128
+         : N == 256  ? JT_R256
+         : N == 512  ? JT_R512
+         : N == 1024 ? JT_R1024
+         : N == 2048 ? JT_R2048
+                     : JT_R4096;
+}
+// the term-split (few-line, latency-bound) launches may use another radix (Cfg::WG instantiations)
+constexpr int radix_ts_of(int64_t N, int maxr) { return maxr <= 2 && N == 128 ? JT_R128_TS : radix_of(N, maxr); }
 template <int N, int MAXR>
 constexpr int radix_for() {
-  return MAXR > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : (N == 2048 ? JT_R2048 : 32)))))));
-}
-int radix_of(int64_t N, int maxr) {
-  return maxr > 2 ? 16 : (N == 16 ? 16 : (N == 32 ? 32 : (N < 256 ? 16 : (N == 256 ? JT_R256 : (N == 512 ? JT_R512 : (N == 4096 ? JT_R4096 : (N == 2048 ? JT_R2048 : 32)))))));
+  return radix_of(N, MAXR);
 }
 
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
@@ -238,12 +250,16 @@ template <int N, int MAXR, bool INV>
 jt_status launch_nmd(const jt_plan_s *p, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
                      const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
   using C = jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, INV>;
-  using CW = jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, INV, true>;
-  if constexpr (CW::LG != C::LG) {  // term-split launches with one-warp groups (Cfg::WG)
+  using CW = jtk::Cfg<N, radix_ts_of(N, MAXR), MAXR, INV, true>;
+  if constexpr (CW::LG != C::LG || CW::R != C::R) {  // term-split launches: one-warp groups / their own radix
     int dev = 0, sms = 148;
     JT_CUDA_TRY(cudaGetDevice(&dev));
     JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (term_split_applies<CW>(ax, nlines, lay, allow_ts, sms)) return launch_cfg<CW>(p, ax, in, out, nlines, lay, s, true);
+    if (term_split_applies<CW>(ax, nlines, lay, allow_ts, sms)) {
+      jtk::AxisDev axt = ax;
+      axt.tw = ax.tw_ts;
+      return launch_cfg<CW>(p, axt, in, out, nlines, lay, s, true);
+    }
   }
   return launch_cfg<C>(p, ax, in, out, nlines, lay, s, allow_ts);
 }
@@ -307,6 +323,7 @@ void free_device(jt_plan_s *p) {
     cudaFree(p->dev[i].ub);
     cudaFree(p->dev[i].v);
     cudaFree(p->dev[i].tw);
+    cudaFree(p->dev[i].tw_ts);
     cudaFree(p->dev[i].phivb);
     cudaFree(p->dev[i].phivc);
     cudaFree(p->dev[i].bstart);
@@ -374,25 +391,30 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   // per-pass twiddle tables (jtk::TwOff): for each pass after the first, at sub-size NS with radix RS,
   // entries (r-1) NS + j = e^{+2 pi i j r / (NS RS)}, computed in long double and rounded once
   const long double PI_L = 3.141592653589793238462643383279502884L;
-  tw.clear();
-  {
-    const int R = radix_of(N, MAXR);
+  auto tw_table = [&](int R) {
+    std::vector<double2> t;
     int64_t NS = std::min<int64_t>(N, R);
     while (NS < N) {
       const int64_t RS = std::min<int64_t>(N / NS, R);
       for (int64_t r = 1; r < RS; ++r)
         for (int64_t j = 0; j < NS; ++j) {
           const long double ang = 2 * PI_L * (long double)(j * r) / (long double)(NS * RS);
-          tw.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+          t.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
         }
       NS *= RS;
     }
-    if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
-  }
+    if (t.empty()) t.push_back(make_double2(1.0, 0.0));
+    return t;
+  };
+  tw = tw_table(radix_of(N, MAXR));
   jt_status s;
   if ((s = upload(&p->dev[axis].ub, ub.data(), ub.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].v, v.data(), v.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].tw, tw.data(), tw.size())) != JT_OK) return s;
+  if (radix_ts_of(N, MAXR) != radix_of(N, MAXR)) {
+    const std::vector<double2> tts = tw_table(radix_ts_of(N, MAXR));
+    if ((s = upload(&p->dev[axis].tw_ts, tts.data(), tts.size())) != JT_OK) return s;
+  }
   if ((s = upload(&p->dev[axis].phivb, phivb.data(), phivb.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].phivc, phivc.data(), phivc.size())) != JT_OK) return s;
   if ((s = upload(&p->dev[axis].bstart, h.bstart.data(), h.bstart.size())) != JT_OK) return s;

@@ -73,11 +73,23 @@
 #endif
 
 // ---- radix and host pipeline (jt_api.cu) -------------------------------------------------------------------
+#ifndef JT_R64
+#define JT_R64 16  // register radix at N = 64 (32: 64^3 inverse +27 %)
+#endif
+#ifndef JT_R128
+#define JT_R128 32  // register radix at N = 128 (32 vs 16: 128^3 forward -7.7 %, inverse -9.5 %)
+#endif
+#ifndef JT_R128_TS
+#define JT_R128_TS 16  // ... in its term-split launches (32 there: 128^2 +30 %)
+#endif
 #ifndef JT_R256
 #define JT_R256 16  // register radix at N = 256 (32: 256^3 inverse -2.3 %, forward +5.6 %, 256^2 +20 %)
 #endif
 #ifndef JT_R512
 #define JT_R512 32  // register radix at N = 512 (16: two exchanges, 26.4 vs 21.7 ms at 512^3)
+#endif
+#ifndef JT_R1024
+#define JT_R1024 32  // register radix at N = 1024
 #endif
 #ifndef JT_R2048
 #define JT_R2048 16  // register radix at N = 2048 (16 vs 32: 2048^2 inverse -6.4 %, forward -0.8 %)

@@ -363,3 +363,16 @@ def test_last_launches_counts_kernels():
     assert jt.jt_last_launches(q) == 2
     torch.cuda.synchronize()
     q.close()
+
+
+@pytest.mark.parametrize("shape,a,b", [((100, 128, 120), (0.3, -0.2, 0.1), (0.2, 0.45, -0.6)),   # many lines: radix 32
+                                       ((128, 96), (0.25, -0.3), (-0.1, 0.4)),                   # term split: radix 16
+                                       ((2000, 3), (0.1, 0.2), (0.3, -0.4))])                    # N = 2048, radix 16
+def test_radix_per_launch_kind(shape, a, b):
+    """FFT lengths whose large launches and term-split launches use different register radixes (N = 128: 32 / 16,
+    with the term-split twiddle tables uploaded separately; tuning.h) against the oracle."""
+    p = jt.Plan(shape, a, b, 1e-12)
+    x = si.gaussian(shape, seed=29)
+    assert relerr(gpu_forward(p, x), oracle.forward(x, a, b)) <= TOL
+    assert relerr(gpu_forward(p, x, inverse=True), oracle.inverse(x, a, b)) <= TOL
+    p.close()
