@@ -86,7 +86,8 @@
 #define JT_R256 16  // register radix at N = 256 (32: 256^3 inverse -2.3 %, forward +5.6 %, 256^2 +20 %)
 #endif
 #ifndef JT_R512
-#define JT_R512 32  // register radix at N = 512 (16: two exchanges, 26.4 vs 21.7 ms at 512^3)
+#define JT_R512 32  // register radix at N = 512 (16: two exchanges, 26.4 vs 21.7 ms at 512^3 before the TMEM work;
+                    // with the current TMEM layouts the radix-16 N = 512 launch configuration is not valid)
 #endif
 #ifndef JT_R1024
 #define JT_R1024 32  // register radix at N = 1024
