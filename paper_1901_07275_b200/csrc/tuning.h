@@ -37,7 +37,7 @@
 #define JT_TWT_LARGE 1  // N > 1024: one TMEM twiddle copy per lane quadrant (4096^2 forward 4.05 -> 3.81 ms)
 #endif
 #ifndef JT_TWT_LARGE_INV_NMAX
-#define JT_TWT_LARGE_INV_NMAX 2048  // ... inverses up to this N (N = 4096 inverse 1 % slower, N = 2048 2 % faster)
+#define JT_TWT_LARGE_INV_NMAX 2048  // ... inverses up to this N (N = 4096 inverse +1..5 % with it, N = 2048 -2 %)
 #endif
 #ifndef JT_TWT_CH_LARGE_F
 #define JT_TWT_CH_LARGE_F 4  // N > 1024 forward: twiddles per TMEM wait (4 vs 8: -5 % at N = 4096)
