@@ -590,7 +590,47 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
   JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_free[slot], 0));
   JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_start, 0));
   const int d = p->d;
-  if (p->dist || d == 1) {  // slabs (with the all-to-all) / one line: copy in, transform, copy out
+  if (p->dist && !inverse) {
+    // distributed forward (transform_dist's schedule, pipelined with the copies): the x-slab arrives in KA row
+    // chunks; each chunk's axes d-1..1 and its rows of the all-to-all run as soon as it is in; the axis-0 pass on
+    // the received y-slab runs in column blocks, each copied back (pitched) while the next computes
+    const int G = p->nranks;
+    const long long n0 = p->n[0], n1 = p->n[1], r = d == 3 ? p->n[2] : 1;
+    const long long R = n0 / G, c = n1 / G, xrow = n1 * r, yrow = c * r;
+    if ((st = ensure_comm_stream(p)) != JT_OK) return st;
+    const int KA = (int)std::min<long long>(4, R);
+    for (int k = 0; k < KA; ++k) {
+      const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
+      if (r1 == r0) continue;
+      const size_t off = (size_t)(r0 * xrow), cnt = (size_t)((r1 - r0) * xrow);
+      JT_CUDA_TRY(cudaMemcpyAsync(sin + off, in_h + off, cnt * sizeof(double), cudaMemcpyHostToDevice, p->s_h2d));
+      JT_CUDA_TRY(cudaEventRecord(ev_in[k], p->s_h2d));
+      JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[k], 0));
+      const double *src1 = sin + off;
+      if (d == 3) {
+        if ((st = launch_axis(p, 2, false, sin + off, sout + off, (r1 - r0) * n1, 1, s)) != JT_OK) return st;
+        src1 = sout + off;
+      }
+      if ((st = launch_axis(p, 1, false, src1, p->a2a_send + r0 * c * r, r1 - r0, r, s, 1, G, -1, true, R)) != JT_OK)
+        return st;
+      JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], s));
+      JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_chunk[k], 0));
+      if ((st = all_to_all_rows(p, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
+    }
+    JT_CUDA_TRY(cudaEventRecord(p->ev_comm, p->s_comm));
+    JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
+    const int KC = (int)std::min<long long>(8, yrow);
+    for (int cb = 0; cb < KC; ++cb) {
+      const long long c0 = yrow * cb / KC, c1 = yrow * (cb + 1) / KC;
+      if (c1 == c0) continue;
+      if ((st = launch_axis(p, 0, false, p->a2a_recv + c0, sout + c0, 1, yrow, s, 1, 1, c1 - c0)) != JT_OK) return st;
+      JT_CUDA_TRY(cudaEventRecord(ev_out[cb], s));
+      JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[cb], 0));
+      JT_CUDA_TRY(cudaMemcpy2DAsync(out_h + c0, (size_t)yrow * sizeof(double), sout + c0, (size_t)yrow * sizeof(double),
+                                    (size_t)(c1 - c0) * sizeof(double), (size_t)n0, cudaMemcpyDeviceToHost,
+                                    p->s_d2h));
+    }
+  } else if (p->dist || d == 1) {  // distributed inverse / one line: copy in, transform, copy out
     JT_CUDA_TRY(cudaMemcpyAsync(sin, in_h, bytes, cudaMemcpyHostToDevice, p->s_h2d));
     JT_CUDA_TRY(cudaEventRecord(ev_in[0], p->s_h2d));
     JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[0], 0));

@@ -286,6 +286,17 @@ class LibSlabPlan:
         jt_forward_host(self.handle, x_host.numpy(), y_host.numpy())
         return y_host
 
+    def forward_host_async(self, x_host, y_host, stream=None):
+        """Enqueue an end-to-end forward of this rank's slab (C: jt_forward_host_async; consecutive calls overlap
+        through the plan's two staging slots); results are valid after wait_host()."""
+        from . import jt_forward_host_async
+        jt_forward_host_async(self.handle, x_host.numpy(), y_host.numpy(), stream)
+        return y_host
+
+    def wait_host(self):
+        from . import jt_host_wait
+        jt_host_wait(self.handle)
+
     def make_forward_step(self, x):
         import torch
         out = torch.empty(self.y_shape, dtype=torch.float64, device=self.device)

@@ -282,6 +282,16 @@ def test_slab_plan_nccl_world1():
                 assert sp.local_box(0) == ((0,) * len(shape), shape)
                 y = sp.forward(sp.local_input(x))
                 assert relerr(y.cpu().numpy(), oracle.forward(x, a, b)) <= TOL, cls
+                if cls is LibSlabPlan:  # the pipelined host-buffer path (row chunks may take the term-split
+                    # launches, which sum the rank terms in another order: equal up to rounding)
+                    xh = sp.local_input(torch.from_numpy(x)).cpu().pin_memory()
+                    yh = [torch.empty(sp.y_shape, dtype=torch.float64).pin_memory() for _ in range(3)]
+                    sp.forward_host(xh, yh[0])
+                    for k in (1, 2):  # two calls in flight through the staging slots
+                        sp.forward_host_async(xh, yh[k])
+                    sp.wait_host()
+                    for k in range(3):
+                        assert relerr(yh[k].numpy(), y.cpu().numpy()) <= 1e-14, k
                 z = sp.inverse(y)
                 assert relerr(z.cpu().numpy(), x) <= TOL, cls
                 sp.close()
