@@ -25,10 +25,10 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-# NCCL_DEBUG=VERSION (the GPU image's default) makes NCCL print its version banner on stdout at communicator
-# creation, ahead of the one JSON line; drop that level only (INFO/TRACE/WARN from the caller are kept)
-if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
-    del os.environ["NCCL_DEBUG"]
+# NCCL's log (NCCL_DEBUG=VERSION is the GPU image's default; INFO shows the communicators' ranks) goes to stderr,
+# so stdout carries only the one JSON line and the driver can still read NCCL's banner and init lines
+if os.environ.get("NCCL_DEBUG") and not os.environ.get("NCCL_DEBUG_FILE"):
+    os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
 sys.path.insert(0, ROOT)
 
 import seeded_inputs as si  # noqa: E402
@@ -318,6 +318,35 @@ def main():
     roofline = None
     per_axis_ms = None
     step_stats = None
+    slab_phases = None
+    if slab:
+        # phase split of the distributed step (jt_profile / jt_last_profile: CUDA events inside the library's
+        # schedule), taken on extra profiled steps AFTER the timed region so the timed steps carry no host syncs
+        jt.jt_profile(plan.handle, True)
+        prof = []
+        for _ in range(max(3, min(args.steps, 10))):
+            step()
+            prof.append(jt.jt_last_profile(plan.handle))
+        jt.jt_profile(plan.handle, False)
+        med = lambda v: float(np.median(v))  # noqa: E731
+        axis_ms = [med([p["axis_ms"][i] for p in prof]) for i in range(3)][:d]
+        slab_phases = {"axis_ms": [round(v, 4) for v in axis_ms], "exchange_ms": round(med([p["exchange_ms"] for p in prof]), 4),
+                       "call_ms": round(med([p["total_ms"] for p in prof]), 4),
+                       "note": "rank-local CUDA events (library jt_profile), median of extra profiled steps after the "
+                               "timed region; axis 1 runs in row chunks overlapped with the all-to-all, so its span "
+                               "and the exchange span overlap"}
+        if dist is not None:
+            t = torch.tensor([slab_phases["call_ms"], slab_phases["exchange_ms"]] + axis_ms, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            slab_phases["max_over_ranks"] = [round(float(v), 4) for v in t.cpu()]
+        # dominant kernel: the axis-0 pass (one whole launch on the received y-slab, n0 x (n1/G)(n2) points)
+        flops = algorithmic_flops_per_point(plan.infos[0]["N"], ranks[0], k0s[0]) * local_points
+        achieved = flops / (axis_ms[0] * 1e-3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                    "kernel": f"fwd_axis_kernel<N={shape[0]}> (axis 0, on this rank's y-slab)",
+                    "flops_per_launch": flops,
+                    "peak_source": "FP64 DFMA measured 37.0 TF/s burst = sustained (profiles/fp64_peak_r01.json)"}
     if not slab:
         per_axis = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(d)] for k in range(args.steps)])
         per_axis_ms = per_axis.mean(axis=0)  # in launch order (axis d-1 first)
@@ -419,6 +448,8 @@ def main():
                 "config": config_block(args, cfg, ranks, k0s), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
                 "ms_per_step_stats": step_stats, "fac_s": round(fac_s, 3)}
+        if slab_phases is not None:
+            line["slab_phases"] = slab_phases
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -23,7 +23,17 @@
  *   - Every call returns a jt_status; no C++ exception crosses the ABI.  On a non-OK status,
  *     jt_last_error() returns a thread-local human-readable message.
  *   - Device-pointer calls enqueue work on `cuda_stream` (a cudaStream_t; NULL = legacy default
- *     stream) and return without synchronising.  One in-flight call per plan at a time.
+ *     stream) and return without synchronising.  Calls on one plan may use different streams: each call's
+ *     first work waits (cudaStreamWaitEvent) for the previous call on the plan to finish with the plan-owned
+ *     buffers (staging, all-to-all, term-split workspace), so calls on one plan never overlap on the device;
+ *     use one plan per concurrent stream for overlap.  Calls on one plan must come from one host thread.
+ *   - Sizes: 2 <= n[i] <= 4096.  The upper bound is the kernels' largest FFT length (one register + two
+ *     shared-memory Stockham passes per line, tables sized for N <= 4096); 4096^3 (550 GB) is reached with
+ *     distributed plans (jt_plan_dist_ex, JT_DIST_LOWMEM on 8 GPUs).
+ *   - Aliasing (in the terms of SURVEY.md §8(b)): device calls take input and output pointers that either
+ *     coincide exactly (in place, allowed for the single-GPU transforms and plain-layout axis passes) or do
+ *     not overlap at all; any partial overlap is JT_ERR_ARG.  Distributed and chunk-major calls must be out
+ *     of place.
  */
 #ifndef JT_H
 #define JT_H
@@ -42,10 +52,12 @@ typedef enum {
                          null pointer, aliasing in/out where not allowed, host-only plan on a device call */
   JT_ERR_DOMAIN = 2,  /* a or b outside (-1, 1): the paper's validated range, "not applicable" outside
                           */
-  JT_ERR_NUMERIC = 3, /* Newton for the nodes did not converge, or the adaptive rank exceeded its cap */
+  JT_ERR_NUMERIC = 3, /* Newton for the nodes did not converge, or the adaptive rank had to grow beyond its growth
+                         cap min(n, n - k0) / 4 (reading R25) */
   JT_ERR_ALLOC = 4,   /* host or device allocation failed */
   JT_ERR_CUDA = 5,    /* a CUDA runtime error (launch, copy, or an asynchronous fault from an earlier call) */
-  JT_ERR_NCCL = 6     /* reserved for the library-owned NCCL path */
+  JT_ERR_NCCL = 6     /* the library-owned NCCL path (distributed plans): libnccl.so.2 missing, a failed call,
+                         or an asynchronous communicator error (the communicator is then aborted) */
 } jt_status;
 
 /* Plan options.  jt_default_opts() fills the defaults shown. */
@@ -167,6 +179,24 @@ jt_status jt_axis_pass_ex(jt_plan_t p, int axis, int inverse, const double *in, 
 jt_status jt_dist_unique_id(void *nccl_unique_id /* 128 bytes, written */);
 jt_status jt_plan_dist(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
                        const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks);
+
+/* jt_plan_dist with flags (0 = jt_plan_dist):
+ *   JT_DIST_LOWMEM  capacity mode (grids larger than one GPU; the paper's memory claim
+ *                   O((r_x + r_y + r_z) n^3), is O(n^3) here): the plan allocates NO slab-sized
+ *                   buffers.  jt_forward / jt_inverse use the caller's INPUT slab as their workspace and the
+ *                   all-to-all runs between the caller's two slabs (not pipelined), so the input's contents are
+ *                   DESTROYED (undefined afterwards); per-GPU memory is the caller's two slabs + the plan's factors
+ *                   (a few MB per axis) + NCCL's own buffers: 4096^3 on 8 GPUs needs 2 x 68.7 GB per GPU.  The
+ *                   *_host variants stage through one plan-owned pair of slabs (copy in, transform, copy out). */
+enum { JT_DIST_LOWMEM = 1 };
+jt_status jt_plan_dist_ex(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
+                          const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks, int flags);
+
+/* Wait until the work enqueued on `cuda_stream` has finished.  On a distributed plan the communicator is polled
+ * meanwhile (ncclCommGetAsyncError): a failed or dead peer returns JT_ERR_NCCL (the communicator is aborted and
+ * every later call on the plan returns JT_ERR_NCCL) instead of hanging.  jt_host_wait and the synchronous *_host
+ * calls wait the same way. */
+jt_status jt_sync(jt_plan_t p, void *cuda_stream);
 /* Index box [lo, hi) of this rank's block: which = 0 the forward input (x-slab), 1 the forward output
  * (y-slab).  Non-distributed plans return the whole array. */
 jt_status jt_local_box(jt_plan_t p, int which, int64_t lo[], int64_t hi[]);
@@ -205,6 +235,17 @@ jt_status jt_plan_sigma(jt_plan_t p, int axis, double *sigma, int *count, int *r
  * partial-sum reduction per axis whose rank terms were split over CTAs (few lines).  Used by bench.py's
  * gpu_launches.  JT_ERR_ARG for a NULL p or count. */
 jt_status jt_last_launches(jt_plan_t p, int *count);
+
+/* Phase timing (bench.py's per-axis and all-to-all split).  jt_profile(p, 1) makes every later jt_forward /
+ * jt_inverse / jt_adjoint on p record CUDA timing events around its phases (a few microseconds per call; 0 turns
+ * it off).  jt_last_profile waits for the most recent such call and returns, in milliseconds:
+ *   ms[0], ms[1], ms[2]  the axis-0 / axis-1 / axis-2 passes (first launch start to last launch end: the
+ *                        distributed schedule runs a pass in row chunks overlapped with the exchange), 0 if absent;
+ *   ms[3]                the all-to-all (distributed plans; first chunk start to last chunk end on its stream);
+ *   ms[4]                the whole call.
+ * JT_ERR_ARG if profiling is off or no profiled call was made. */
+jt_status jt_profile(jt_plan_t p, int enable);
+jt_status jt_last_profile(jt_plan_t p, double ms[5]);
 
 /* Thread-local text of the last non-OK status ("" if none). */
 const char *jt_last_error(void);

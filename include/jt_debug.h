@@ -17,6 +17,40 @@ extern "C" {
 #endif
 jt_status jt_debug_modified_pq(double a, double b, int64_t nt, const double *t, int kmax, double *p_out,
                                double *q_out);
+
+/* Virtual ranks on one GPU (tests of the distributed schedule, with only one GPU at hand).
+ *
+ * jt_debug_vgroup_create makes a group of `nranks` virtual ranks; jt_debug_plan_virtual then builds rank `rank`'s
+ * distributed plan exactly as jt_plan_dist_ex does (same n / a / b / eps / opts / flags on every rank, same
+ * x-slab / y-slab boxes, same schedule, same kernels, same chunk-major layouts), except that the all-to-all is
+ * not NCCL: rank g's exchange copies rows of block g of every member's send buffer into its own receive buffer
+ * with one cudaMemcpyAsync per peer on its own stream, ordered by cross-stream CUDA events and a host barrier
+ * of the G members (so the G ranks must be driven by G host threads, each calling jt_forward / jt_inverse /
+ * jt_*_host* on its own plan and stream, like G processes would).  No kernel waits on another: the copies are
+ * ordinary stream work.  A member that does not reach an exchange within `timeout_ms` makes the others' call
+ * return JT_ERR_NCCL and marks their plans broken (the communicator-abort path of the NCCL build).
+ * All members must use the same device.  Destroy every member plan (jt_destroy) before the group.
+ * Errors: JT_ERR_ARG for bad sizes, a NULL group, a rank that already has a plan, or destroying a group that
+ * still has plans. */
+/* Bounds-check build (libjt_checks.so, compiled with -DJT_CHECKS=1 by build.py): every global index, shared-memory
+ * exchange slot, bin index and tensor-memory column the kernels touch is checked; a violation is counted and its
+ * access skipped (no fault).  jt_debug_checks synchronises the device and returns whether this build checks
+ * (*enabled), the number of violations since the last call (*count) and the kernel source line of the first
+ * (*line), then resets both.  JT_ERR_ARG on NULL arguments. */
+jt_status jt_debug_checks(int *enabled, unsigned long long *count, int *line);
+
+/* jt_forward_axis / jt_inverse_axis (plain layout, out of place or in place, never term-split) with the input and
+ * output extents DECLARED by the caller (elements from the pointers) instead of derived from the geometry: the
+ * negative control of the checks build (declaring out_lim smaller than outer * n[axis] * inner must produce
+ * violations and leave the elements beyond out_lim untouched). */
+jt_status jt_debug_axis_pass_lim(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
+                                 int64_t inner, int64_t in_lim, int64_t out_lim, void *cuda_stream);
+
+typedef struct jt_vgroup_s *jt_vgroup_t;
+jt_status jt_debug_vgroup_create(jt_vgroup_t *out, int nranks, int timeout_ms);
+jt_status jt_debug_vgroup_destroy(jt_vgroup_t group);
+jt_status jt_debug_plan_virtual(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
+                                double eps, const jt_opts *opts, jt_vgroup_t group, int rank, int flags);
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,11 @@ EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_k
             "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
             "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_axis_pass_ex", "jt_destroy", "jt_plan_rank", "jt_plan_info",
             "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_launches", "jt_last_error", "jt_version",
-            "jt_debug_modified_pq"]
+            "jt_plan_dist_ex", "jt_sync", "jt_profile", "jt_last_profile",
+            "jt_debug_modified_pq", "jt_debug_checks", "jt_debug_vgroup_create", "jt_debug_vgroup_destroy",
+            "jt_debug_plan_virtual", "jt_debug_axis_pass_lim"]
+
+JT_DIST_LOWMEM = 1
 
 
 class JTError(RuntimeError):
@@ -61,6 +65,20 @@ _lib.jt_plan_ex.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctyp
 _lib.jt_dist_unique_id.argtypes = [ctypes.c_void_p]
 _lib.jt_plan_dist.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double, ctypes.POINTER(jt_opts),
                               ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+_lib.jt_plan_dist_ex.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double,
+                                 ctypes.POINTER(jt_opts), ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+_lib.jt_sync.argtypes = [_P, ctypes.c_void_p]
+_lib.jt_profile.argtypes = [_P, ctypes.c_int]
+_lib.jt_last_profile.argtypes = [_P, _D]
+_lib.jt_debug_checks.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_ulonglong),
+                                 ctypes.POINTER(ctypes.c_int)]
+_lib.jt_debug_vgroup_create.argtypes = [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int]
+_lib.jt_debug_vgroup_destroy.argtypes = [_P]
+_lib.jt_debug_plan_virtual.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double,
+                                       ctypes.POINTER(jt_opts), _P, ctypes.c_int, ctypes.c_int]
+_lib.jt_debug_axis_pass_lim.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_void_p]
 _lib.jt_local_box.argtypes = [_P, ctypes.c_int, _I64, _I64]
 _lib.jt_plan_kind.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
 _lib.jt_host_wait.argtypes = [_P]
@@ -105,6 +123,35 @@ def _ptr(x) -> int:
     if x.dtype.__repr__() != "torch.float64" or not x.is_contiguous():
         raise ValueError("tensors must be contiguous torch.float64")
     return x.data_ptr()
+
+
+def _local_elems(plan: int, which: int) -> int:
+    """Elements of the plan's local array: which = 0 the forward input (x-slab), 1 the forward output (y-slab);
+    the whole array for non-distributed plans (C: jt_local_box)."""
+    lo = (ctypes.c_int64 * 3)(0, 0, 0)
+    hi = (ctypes.c_int64 * 3)(1, 1, 1)
+    _check(_lib.jt_local_box(plan, which, lo, hi), "jt_local_box")
+    return int(np.prod([h - l for l, h in zip(lo, hi)]))
+
+
+def _host_ptr(x, plan: int, which: int) -> int:
+    """Address of a host buffer of a *_host call after checking it: a C-contiguous float64 numpy array with exactly
+    the plan's local element count (the C side reads / writes that many doubles)."""
+    if not isinstance(x, np.ndarray):
+        raise TypeError("host buffers must be numpy arrays (e.g. tensor.numpy() of a pinned CPU tensor)")
+    if x.dtype != np.float64 or not x.flags.c_contiguous:
+        raise ValueError("host buffers must be C-contiguous float64")
+    want = _local_elems(plan, which)
+    if x.size != want:
+        raise ValueError(f"host buffer has {x.size} elements, the plan's local array has {want}")
+    if not x.flags.writeable and which == 1:
+        raise ValueError("output host buffer is read-only")
+    return x.ctypes.data
+
+
+# Host buffers of *_host_async calls in flight, per plan handle: kept alive until jt_host_wait (the copies read /
+# write them asynchronously).
+_INFLIGHT: dict = {}
 
 
 def _stream_handle(stream) -> int:
@@ -186,8 +233,8 @@ def jt_dist_unique_id() -> bytes:
 
 
 def jt_plan_dist(n, a, b, eps: float, uid: bytes, rank: int, nranks: int, seed: int = 0, k0: int = -1,
-                 device: int = -1) -> int:
-    """Slab-distributed plan with a library-owned NCCL communicator (C: jt_plan_dist)."""
+                 device: int = -1, flags: int = 0) -> int:
+    """Slab-distributed plan with a library-owned NCCL communicator (C: jt_plan_dist_ex; flags JT_DIST_LOWMEM)."""
     n = [int(v) for v in np.atleast_1d(n)]
     d = len(n)
     a = np.broadcast_to(np.asarray(a, dtype=np.float64), (d,)).copy()
@@ -198,8 +245,9 @@ def jt_plan_dist(n, a, b, eps: float, uid: bytes, rank: int, nranks: int, seed: 
         raise ValueError("uid must be the 128-byte NCCL unique id")
     h = _P()
     idbuf = ctypes.create_string_buffer(bytes(uid), 128)
-    _check(_lib.jt_plan_dist(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D),
-                             b.ctypes.data_as(_D), float(eps), ctypes.byref(o), idbuf, rank, nranks), "jt_plan_dist")
+    _check(_lib.jt_plan_dist_ex(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D),
+                                b.ctypes.data_as(_D), float(eps), ctypes.byref(o), idbuf, rank, nranks, flags),
+           "jt_plan_dist_ex")
     return h.value
 
 
@@ -221,27 +269,89 @@ def jt_plan_kind(plan: int, axis: int):
 
 
 def jt_forward_host(plan: int, coeffs_host: np.ndarray, values_host: np.ndarray, stream=None):
-    _check(_lib.jt_forward_host(plan, _ptr(coeffs_host), _ptr(values_host), _stream_handle(stream)),
-           "jt_forward_host")
+    _check(_lib.jt_forward_host(plan, _host_ptr(coeffs_host, plan, 0), _host_ptr(values_host, plan, 1),
+                                _stream_handle(stream)), "jt_forward_host")
 
 
 def jt_inverse_host(plan: int, values_host: np.ndarray, coeffs_host: np.ndarray, stream=None):
-    _check(_lib.jt_inverse_host(plan, _ptr(values_host), _ptr(coeffs_host), _stream_handle(stream)),
-           "jt_inverse_host")
+    _check(_lib.jt_inverse_host(plan, _host_ptr(values_host, plan, 1), _host_ptr(coeffs_host, plan, 0),
+                                _stream_handle(stream)), "jt_inverse_host")
 
 
 def jt_forward_host_async(plan: int, coeffs_host: np.ndarray, values_host: np.ndarray, stream=None):
-    _check(_lib.jt_forward_host_async(plan, _ptr(coeffs_host), _ptr(values_host), _stream_handle(stream)),
-           "jt_forward_host_async")
+    a, b = _host_ptr(coeffs_host, plan, 0), _host_ptr(values_host, plan, 1)
+    _check(_lib.jt_forward_host_async(plan, a, b, _stream_handle(stream)), "jt_forward_host_async")
+    _INFLIGHT.setdefault(plan, []).append((coeffs_host, values_host))
 
 
 def jt_inverse_host_async(plan: int, values_host: np.ndarray, coeffs_host: np.ndarray, stream=None):
-    _check(_lib.jt_inverse_host_async(plan, _ptr(values_host), _ptr(coeffs_host), _stream_handle(stream)),
-           "jt_inverse_host_async")
+    a, b = _host_ptr(values_host, plan, 1), _host_ptr(coeffs_host, plan, 0)
+    _check(_lib.jt_inverse_host_async(plan, a, b, _stream_handle(stream)), "jt_inverse_host_async")
+    _INFLIGHT.setdefault(plan, []).append((values_host, coeffs_host))
 
 
 def jt_host_wait(plan: int):
-    _check(_lib.jt_host_wait(plan), "jt_host_wait")
+    try:
+        _check(_lib.jt_host_wait(plan), "jt_host_wait")
+    finally:
+        _INFLIGHT.pop(plan, None)
+
+
+def jt_sync(plan: int, stream=None):
+    """Wait for `stream`, polling a distributed plan's communicator (JT_ERR_NCCL instead of a hang)."""
+    _check(_lib.jt_sync(plan, _stream_handle(stream)), "jt_sync")
+
+
+def jt_profile(plan: int, enable: bool = True):
+    _check(_lib.jt_profile(plan, int(bool(enable))), "jt_profile")
+
+
+def jt_last_profile(plan: int) -> dict:
+    """Phase times (ms) of the most recent profiled transform: axis passes 0/1/2, the all-to-all, the whole call."""
+    ms = (ctypes.c_double * 5)()
+    _check(_lib.jt_last_profile(plan, ms), "jt_last_profile")
+    return {"axis_ms": [ms[0], ms[1], ms[2]], "exchange_ms": ms[3], "total_ms": ms[4]}
+
+
+def jt_debug_checks():
+    """(enabled, violations since the last call, source line of the first) of the bounds-checked build."""
+    e, c, ln = ctypes.c_int(), ctypes.c_ulonglong(), ctypes.c_int()
+    _check(_lib.jt_debug_checks(ctypes.byref(e), ctypes.byref(c), ctypes.byref(ln)), "jt_debug_checks")
+    return bool(e.value), int(c.value), int(ln.value)
+
+
+def jt_debug_axis_pass_lim(plan: int, axis: int, inverse: bool, x_in, x_out, outer: int, inner: int, in_lim: int,
+                           out_lim: int, stream=None):
+    """Axis pass with caller-declared buffer extents (include/jt_debug.h): the checks build's negative control."""
+    _check(_lib.jt_debug_axis_pass_lim(plan, axis, int(bool(inverse)), _ptr(x_in), _ptr(x_out), outer, inner, in_lim,
+                                       out_lim, _stream_handle(stream)), "jt_debug_axis_pass_lim")
+
+
+def jt_debug_vgroup_create(nranks: int, timeout_ms: int = 120000) -> int:
+    g = _P()
+    _check(_lib.jt_debug_vgroup_create(ctypes.byref(g), nranks, timeout_ms), "jt_debug_vgroup_create")
+    return g.value
+
+
+def jt_debug_vgroup_destroy(group: int):
+    _check(_lib.jt_debug_vgroup_destroy(group), "jt_debug_vgroup_destroy")
+
+
+def jt_debug_plan_virtual(n, a, b, eps: float, group: int, rank: int, flags: int = 0, seed: int = 0,
+                          k0: int = -1, device: int = -1) -> int:
+    """Rank `rank`'s distributed plan in a virtual group (include/jt_debug.h): the library's slab schedule with an
+    in-process exchange instead of NCCL (tests on one GPU)."""
+    n = [int(v) for v in np.atleast_1d(n)]
+    d = len(n)
+    a = np.broadcast_to(np.asarray(a, dtype=np.float64), (d,)).copy()
+    b = np.broadcast_to(np.asarray(b, dtype=np.float64), (d,)).copy()
+    o = jt_default_opts()
+    o.seed, o.k0, o.device = seed, k0, device
+    h = _P()
+    _check(_lib.jt_debug_plan_virtual(ctypes.byref(h), d, (ctypes.c_int64 * d)(*n), a.ctypes.data_as(_D),
+                                      b.ctypes.data_as(_D), float(eps), ctypes.byref(o), group, rank, flags),
+           "jt_debug_plan_virtual")
+    return h.value
 
 
 def jt_forward_axis(plan: int, axis: int, x_in, x_out, outer: int, inner: int, stream=None):
@@ -269,7 +379,10 @@ def jt_axis_pass_ex(plan: int, axis: int, inverse: bool, x_in, x_out, outer: int
 
 
 def jt_destroy(plan: int):
-    _check(_lib.jt_destroy(plan), "jt_destroy")
+    try:
+        _check(_lib.jt_destroy(plan), "jt_destroy")
+    finally:
+        _INFLIGHT.pop(plan, None)
 
 
 def jt_plan_rank(plan: int, axis: int) -> int:
@@ -359,13 +472,13 @@ class Plan:
         return jt_plan_kind(self.handle, axis)
 
     def forward_host(self, coeffs: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
-        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64).reshape(self.shape)
         out = np.empty(self.shape) if out is None else out
         jt_forward_host(self.handle, coeffs, out, stream)
         return out
 
     def inverse_host(self, values: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
-        values = np.ascontiguousarray(values, dtype=np.float64)
+        values = np.ascontiguousarray(values, dtype=np.float64).reshape(self.shape)
         out = np.empty(self.shape) if out is None else out
         jt_inverse_host(self.handle, values, out, stream)
         return out

@@ -70,6 +70,25 @@ struct TermSplit {
 
 // (build-time tuning knobs JT_*: tuning.h)
 
+// ---- JT_CHECKS builds (build.py `checks`: libjt_checks.so): bounds checks on every global index, shared-memory
+// slot and tensor-memory column the kernels touch.  A violation is counted (jt_check_count, the first one's
+// source line in jt_check_line; read by jt_debug_checks) and the access is SKIPPED, so a checks run never
+// faults the GPU (the substitute for compute-sanitizer, which is closed on this pool).  Off: JT_CHK(c) is true.
+#ifndef JT_CHECKS
+#define JT_CHECKS 0
+#endif
+__device__ unsigned long long jt_check_count;
+__device__ int jt_check_line;
+__device__ __forceinline__ bool chk(bool ok, int line) {
+  if (!ok && atomicAdd(&jt_check_count, 1ull) == 0ull) jt_check_line = line;
+  return ok;
+}
+#if JT_CHECKS
+#define JT_CHK(cond) (::jtk::chk((cond), __LINE__))
+#else
+#define JT_CHK(cond) true
+#endif
+
 constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
 constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
                             // (4 measured slower: a bigger stage leaves room for only 2 ring stages)
@@ -322,6 +341,10 @@ struct Ring {
     const int l = l0 + (int)(seq % rs);
     const bool kc = C::VST && l * C::KPT < k0;  // chunk l of W V exists (zero-padded to KPT degrees)
     const uint32_t ph_bytes = kc ? C::PH_BYTES : 0;
+    if (!JT_CHK(l >= 0 && l < r)) {  // (checks build: complete the phase without copying, so nobody hangs)
+      mbar_arrive_expect_tx(&full[s], 0);
+      return;
+    }
     mbar_arrive_expect_tx(&full[s], C::SV_BYTES + C::U_BYTES + ph_bytes);
     if constexpr (C::STAGED) tma_load_1d(v(seq), gv + (long long)l * C::N, C::V_BYTES, &full[s]);
     tma_load_1d(u(seq), gu + (long long)l * C::MAXR * C::NBINS, C::U_BYTES, &full[s]);
@@ -370,6 +393,7 @@ __device__ __forceinline__ void pass_store(const double (&xr)[C::R], const doubl
 #pragma unroll
     for (int s = 0; s < P::RS; ++s) {
       const int sl = C::sidx(idxD + s * NS, line);
+      if (!JT_CHK(sl >= 0 && sl < C::SLOTS)) continue;
       if constexpr (C::SPLITX) {
         static_cast<double *>(buf)[sl] = plane == 0 ? xr[i * P::RS + s] : xi[i * P::RS + s];
       } else {
@@ -391,6 +415,7 @@ __device__ __forceinline__ void pass_load(double (&xr)[C::R], double (&xi)[C::R]
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
       const int sl = C::sidx(v + r * (C::N / RS), line);
+      if (!JT_CHK(sl >= 0 && sl < C::SLOTS)) continue;
       if constexpr (C::SPLITX) {
         if (plane == 0) xr[i * RS + r] = static_cast<const double *>(buf)[sl];
         else xi[i * RS + r] = static_cast<const double *>(buf)[sl];
@@ -673,6 +698,7 @@ struct Ctx {
     }
     if constexpr (C::STAGED) for (int i = threadIdx.x; i < C::TPL * C::NB; i += C::NT) {
       const int m = binof(i / C::NB, i % C::NB);
+      if (!JT_CHK(m >= 0 && m < C::NBINS)) continue;
       const int j0 = __ldg(&bstart[m]);
       binfo()[i] = (j0 << 4) | (__ldg(&bstart[m + 1]) - j0);
     }
@@ -698,7 +724,8 @@ struct Ctx {
         for (int i = 2 * C::TWPT; i < NV; ++i) t[i] = 0.0;
         tw_fill<C, Pass<C::N, C::R, 1>::RS>(t, vt, tw);
 #pragma unroll
-        for (int c = 0; c < NV / 8; ++c) tmem_st_d8(ttw + 16 * c, &t[8 * c]);
+        for (int c = 0; c < NV / 8; ++c)
+          if (JT_CHK((int)(ttw & 0xffff) + 16 * c + 16 <= C::TALLOC)) tmem_st_d8(ttw + 16 * c, &t[8 * c]);
         tmem_wait_st();
       }
       if constexpr (C::TW_SHARED) {
@@ -753,6 +780,7 @@ struct State {
     } else if constexpr (C::TPRIV) {
 #pragma unroll
       for (int c = 0; c < 2 * NCH; ++c) {  // 8 doubles (16 columns) per store, zero padded
+        if (!JT_CHK((int)(taddr & 0xffff) + 16 * c + 16 <= C::TALLOC)) continue;
         double t[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) t[i] = (c * 8 + i < S) ? v[c * 8 + i] : 0.0;
@@ -767,6 +795,7 @@ struct State {
   // TMEM state only: chunk c's loads issued, the caller waits (tmem_wait_ld) before reading o
   __device__ __forceinline__ void chunk_issue(int c, double (&o)[CH]) const {
     static_assert(C::TPRIV, "chunk_issue reads the TMEM state");
+    JT_CHK((int)(taddr & 0xffff) + 32 * c + 32 <= C::TALLOC);
     tmem_ld_d8(taddr + 32 * c, &o[0]);
     tmem_ld_d8(taddr + 32 * c + 16, &o[8]);
   }
@@ -775,6 +804,7 @@ struct State {
 #pragma unroll
       for (int i = 0; i < CH; ++i) o[i] = (c * CH + i < S) ? reg[c * CH + i] : 0.0;
     } else if constexpr (C::TPRIV) {
+      JT_CHK((int)(taddr & 0xffff) + 32 * c + 32 <= C::TALLOC);
       tmem_ld_d8(taddr + 32 * c, &o[0]);
       tmem_ld_d8(taddr + 32 * c + 16, &o[8]);
       tmem_wait_ld();
@@ -801,6 +831,7 @@ struct Layout {
   int in_cs, out_cs;  // chunk length of the input / output along the axis (== n: plain C-order)
   long long ostride;  // outer extent of the chunk-major blocks (== outer, or the whole slab when a launch
                       // covers only part of its rows: the pipelined all-to-all of the distributed forward)
+  long long in_lim, out_lim;  // elements readable / writable from the in / out pointers (JT_CHECKS builds)
 };
 
 
@@ -875,13 +906,15 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int k = vt + r * TPL;
-        av[r] = (live && k < n) ? __ldg(&in[ia.at(k)]) : 0.0;
+        av[r] = (live && k < n && JT_CHK(ia.at(k) >= 0 && ia.at(k) < lay.in_lim)) ? __ldg(&in[ia.at(k)]) : 0.0;
       }
       a.store(av);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int k = vt + r * TPL;
         if (r * TPL < K0MAX && k < K0MAX) cx.alow[k * LG + line] = k < k0 ? av[r] : 0.0;  // zero pad: W V pairs
+        // (checks: the bins every thread reads are real FFT bins)
+        if (r < NB) JT_CHK(m[r] >= 0 && m[r] < NBINS);
       }
     }
     prefetch_next_line<C, SPLIT>(in, lay, ((bt + cx.btstep) * C::GPC + cx.grp) * LG + line, nlines, vt, n);
@@ -991,9 +1024,9 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
           cx.rows_of(ax.bstart, q, m[q], j0, cnt);
 #pragma unroll
           for (int c = 0; c < MAXR; ++c)
-            if (c < cnt) {
+            if (c < cnt && JT_CHK(j0 + c >= 0 && j0 + c < n && L < nlines)) {
               if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + j0 + c] = y[q][c];
-              else out[oa.at(j0 + c)] = y[q][c];
+              else if (JT_CHK(oa.at(j0 + c) >= 0 && oa.at(j0 + c) < lay.out_lim)) out[oa.at(j0 + c)] = y[q][c];
             }
         }
       }
@@ -1043,7 +1076,11 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         int j0, cnt;
         cx.rows_of(ax.bstart, q, m[q], j0, cnt);
 #pragma unroll
-        for (int c = 0; c < MAXR; ++c) yr[q * MAXR + c] = (live && own && c < cnt) ? __ldg(&in[ia.at(j0 + c)]) : 0.0;
+        for (int c = 0; c < MAXR; ++c)
+          yr[q * MAXR + c] = (live && own && c < cnt && JT_CHK(j0 + c < n && m[q] < NBINS) &&
+                              JT_CHK(ia.at(j0 + c) >= 0 && ia.at(j0 + c) < lay.in_lim))
+                                 ? __ldg(&in[ia.at(j0 + c)])
+                                 : 0.0;
       }
       yb.store(yr);
       prefetch_next_line<C, SPLIT>(in, lay, ((bt + cx.btstep) * C::GPC + cx.grp) * LG + line, nlines, vt, n);
@@ -1196,7 +1233,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         if (k < k0) val += cx.alow[k * LG + line];
         if (k < n) {
           if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + k] = val;
-          else out[oa.at(k)] = val;
+          else if (JT_CHK(oa.at(k) >= 0 && oa.at(k) < lay.out_lim)) out[oa.at(k)] = val;
         }
       }
     }

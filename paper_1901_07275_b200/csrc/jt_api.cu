@@ -6,13 +6,19 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "axis_kernels.cuh"
+#include "jt_debug.h"
 #include "jt_internal.h"
 
 // (JT_HOST_SLOTS, JT_R512, JT_R4096: tuning.h.)  The *_host entry points rotate through JT_HOST_SLOTS staging
@@ -60,13 +66,15 @@ struct DeviceGuard {
 namespace nccl {
 typedef struct { char internal[128]; } UniqueId;
 typedef void *Comm;
-enum { Success = 0, Float64 = 8 };
+enum { Success = 0, Float64 = 8, InProgress = 7 };
 struct Api {
   bool ok = false;
   std::string why;
   int (*GetUniqueId)(UniqueId *) = nullptr;
   int (*CommInitRank)(Comm *, int, UniqueId, int) = nullptr;
   int (*CommDestroy)(Comm) = nullptr;
+  int (*CommAbort)(Comm) = nullptr;
+  int (*CommGetAsyncError)(Comm, int *) = nullptr;
   int (*Send)(const void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*Recv)(void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*GroupStart)() = nullptr;
@@ -84,13 +92,15 @@ Api &api() {
     r.GetUniqueId = (int (*)(UniqueId *))dlsym(h, "ncclGetUniqueId");
     r.CommInitRank = (int (*)(Comm *, int, UniqueId, int))dlsym(h, "ncclCommInitRank");
     r.CommDestroy = (int (*)(Comm))dlsym(h, "ncclCommDestroy");
+    r.CommAbort = (int (*)(Comm))dlsym(h, "ncclCommAbort");
+    r.CommGetAsyncError = (int (*)(Comm, int *))dlsym(h, "ncclCommGetAsyncError");
     r.Send = (int (*)(const void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclSend");
     r.Recv = (int (*)(void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclRecv");
     r.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
     r.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
     r.GetErrorString = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
-    r.ok = r.GetUniqueId && r.CommInitRank && r.CommDestroy && r.Send && r.Recv && r.GroupStart && r.GroupEnd &&
-           r.GetErrorString;
+    r.ok = r.GetUniqueId && r.CommInitRank && r.CommDestroy && r.CommAbort && r.CommGetAsyncError && r.Send &&
+           r.Recv && r.GroupStart && r.GroupEnd && r.GetErrorString;
     if (!r.ok) r.why = "libnccl.so.2 lacks a required symbol";
     return r;
   }();
@@ -117,15 +127,59 @@ struct jt_plan_s {
   mutable int launches = 0;  // kernels enqueued by the latest transform call (jt_last_launches)
   // slab-distributed plans (jt_plan_dist): this rank's x-slab (forward input) / y-slab
   // (forward output) of the global n[0] x n[1] (x n[2]) array, the all-to-all buffers and the NCCL comm
-  // term-split workspace (few-line launches, jtk::TermSplit)
+  // term-split workspace (few-line launches, jtk::TermSplit); grown stream-ordered (cudaMallocAsync)
   mutable double *ts_work = nullptr;
   mutable size_t ts_elems = 0;
   bool dist = false;
   int rank = 0, nranks = 1;
+  int dist_flags = 0;      // JT_DIST_* (jt_plan_dist_ex)
   nccl::Comm comm = nullptr;
-  double *a2a_send = nullptr, *a2a_recv = nullptr;
+  jt_vgroup_s *vgroup = nullptr;  // test-only in-process exchange (include/jt_debug.h) instead of NCCL
+  bool broken = false;     // a failed exchange aborted the communicator: every later call is JT_ERR_NCCL
+  double *a2a_send = nullptr, *a2a_recv = nullptr;  // (not allocated with JT_DIST_LOWMEM)
   mutable cudaStream_t s_comm = nullptr;  // the pipelined all-to-all's stream (created on first use)
   mutable cudaEvent_t ev_chunk[8] = {}, ev_comm = nullptr;
+  // plan-owned buffers (staging, all-to-all, term-split workspace) are reused by every call: a call's first
+  // work waits for the previous call's last use (recorded at its end), whatever streams the two calls use
+  mutable cudaEvent_t ev_busy = nullptr;
+  // phase timing (jt_profile / jt_last_profile): timing events, recorded by transform / transform_dist
+  bool prof_on = false;
+  mutable cudaEvent_t pev[10] = {};
+  mutable bool prec[10] = {};
+};
+
+// Test-only virtual exchange group (include/jt_debug.h): G plans on ONE device, each driven by its own host
+// thread and stream, exchange their all-to-all blocks by cudaMemcpyAsync between their buffers, ordered by
+// cross-stream events and a host barrier (no kernel waits on another: the copies are plain stream work).
+struct jt_vgroup_s {
+  int G = 0;
+  int timeout_ms = 120000;
+  std::vector<jt_plan_s *> member;      // by rank
+  std::vector<const double *> send;     // each member's send buffer of the exchange in progress
+  std::vector<cudaEvent_t> ev_ready, ev_done;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool failed = false;
+  // all G members arrive (or the group is marked failed after timeout_ms)
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (failed) return false;
+    const unsigned long long g = gen;
+    if (++arrived == G) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::milliseconds(timeout_ms), [&] { return gen != g || failed; }) || failed) {
+      failed = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
 };
 
 namespace {
@@ -191,10 +245,12 @@ jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
     const size_t need = (size_t)S * nlines * ax.n;
     if (S > 1) {
       if (p->ts_elems < need) {
-        cudaFree(p->ts_work);
+        // stream-ordered: no implicit device synchronisation in the middle of a pipelined call (a ragged later
+        // chunk may need more than an earlier one), and valid under CUDA graph capture
+        if (p->ts_work) cudaFreeAsync(p->ts_work, s);
         p->ts_work = nullptr;
         p->ts_elems = 0;
-        if (cudaMalloc((void **)&p->ts_work, need * sizeof(double)) != cudaSuccess)
+        if (cudaMallocAsync((void **)&p->ts_work, need * sizeof(double), s) != cudaSuccess)
           return fail(JT_ERR_ALLOC, "term-split workspace");
         p->ts_elems = need;
       }
@@ -280,15 +336,21 @@ jt_status launch_n(const jt_plan_s *p, bool inverse, int maxr, const jtk::AxisDe
 
 // One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
 // layout of the slab all-to-all for the input / output.
+// in_lim / out_lim: elements of the input / output buffers from the given pointers (bounds of the JT_CHECKS
+// build; -1: the extent the geometry addresses).
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
                       long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
-                      long long nlines_only = -1, bool allow_ts = true, long long ostride = -1) {
+                      long long nlines_only = -1, bool allow_ts = true, long long ostride = -1,
+                      long long in_lim = -1, long long out_lim = -1) {
   jtk::AxisDev ax = axis_dev(p, axis);
   const int maxr = p->dev[axis].maxr;
   // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
   const long long nlines = nlines_only >= 0 ? nlines_only : outer * inner;
-  const jtk::Layout lay{outer, inner, (int)(p->n[axis] / in_split), (int)(p->n[axis] / out_split),
-                        ostride >= 0 ? ostride : outer};
+  const long long ost = ostride >= 0 ? ostride : outer;
+  const long long n = p->n[axis];
+  const long long geo_in = (in_split > 1 ? ost : outer) * n * inner, geo_out = (out_split > 1 ? ost : outer) * n * inner;
+  const jtk::Layout lay{outer, inner, (int)(n / in_split), (int)(n / out_split), ost,
+                        in_lim >= 0 ? in_lim : geo_in, out_lim >= 0 ? out_lim : geo_out};
   switch (ax.N) {
     case 16: return launch_n<16>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
     case 32: return launch_n<32>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
@@ -341,7 +403,17 @@ void free_device(jt_plan_s *p) {
   cudaFree(p->a2a_send);
   cudaFree(p->a2a_recv);
   p->a2a_send = p->a2a_recv = nullptr;
-  if (p->comm) nccl::api().CommDestroy(p->comm), p->comm = nullptr;
+  if (p->comm) (p->broken ? nccl::api().CommAbort(p->comm) : nccl::api().CommDestroy(p->comm)), p->comm = nullptr;
+  if (p->vgroup) {
+    std::lock_guard<std::mutex> lk(p->vgroup->mu);
+    p->vgroup->member[p->rank] = nullptr;
+    if (p->vgroup->ev_ready[p->rank]) cudaEventDestroy(p->vgroup->ev_ready[p->rank]), p->vgroup->ev_ready[p->rank] = nullptr;
+    if (p->vgroup->ev_done[p->rank]) cudaEventDestroy(p->vgroup->ev_done[p->rank]), p->vgroup->ev_done[p->rank] = nullptr;
+    p->vgroup = nullptr;
+  }
+  if (p->ev_busy) cudaEventDestroy(p->ev_busy), p->ev_busy = nullptr;
+  for (auto &e : p->pev)
+    if (e) cudaEventDestroy(e), e = nullptr;
   for (auto &e : p->ev_chunk)
     if (e) cudaEventDestroy(e), e = nullptr;
   if (p->ev_comm) cudaEventDestroy(p->ev_comm), p->ev_comm = nullptr;
@@ -427,9 +499,34 @@ bool overlaps_partially(const double *x, const double *y, int64_t count) {
   return x < ye && y < xe;
 }
 
+// Abort the plan's communicator after a failed or hung exchange (peers blocked on chunks this rank will never
+// post get an error from their own communicator instead of hanging), and refuse every later call.
+jt_status mark_broken(const jt_plan_s *p, const std::string &msg) {
+  jt_plan_s *q = const_cast<jt_plan_s *>(p);
+  if (q->comm && !q->broken) nccl::api().CommAbort(q->comm), q->comm = nullptr;
+  q->broken = true;
+  return fail(JT_ERR_NCCL, msg);
+}
+
+// Asynchronous NCCL errors of a distributed plan (a dead or failed peer): JT_ERR_NCCL and abort.
+jt_status poll_comm(const jt_plan_s *p) {
+  if (p->broken) return fail(JT_ERR_NCCL, "the plan's communicator was aborted after an earlier exchange failure");
+  if (!p->comm) return JT_OK;
+  int ae = nccl::Success;
+  const int e = nccl::api().CommGetAsyncError(p->comm, &ae);
+  if (e != nccl::Success) return mark_broken(p, std::string("ncclCommGetAsyncError: ") + nccl::api().GetErrorString(e));
+  if (ae != nccl::Success && ae != nccl::InProgress)
+    return mark_broken(p, std::string("asynchronous NCCL error: ") + nccl::api().GetErrorString(ae));
+  return JT_OK;
+}
+
 jt_status check_device_plan(const jt_plan_s *p) {
   if (!p) return fail(JT_ERR_ARG, "null plan");
   if (p->device < 0) return fail(JT_ERR_ARG, "host-only plan (opts.device == -2) cannot run device calls");
+  if (p->dist) {
+    jt_status st = poll_comm(p);
+    if (st != JT_OK) return st;
+  }
   // surface an asynchronous fault from an earlier call
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
@@ -437,6 +534,34 @@ jt_status check_device_plan(const jt_plan_s *p) {
     return fail(JT_ERR_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(e));
   }
   return JT_OK;
+}
+
+// Ordering of calls that share the plan-owned buffers: the call's stream waits for the previous call's end.
+jt_status begin_call(const jt_plan_s *p, cudaStream_t s) {
+  if (!p->ev_busy) {
+    JT_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_busy, cudaEventDisableTiming));
+    JT_CUDA_TRY(cudaEventRecord(p->ev_busy, s));
+  }
+  JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_busy, 0));
+  return JT_OK;
+}
+jt_status end_call(const jt_plan_s *p, cudaStream_t s) {
+  JT_CUDA_TRY(cudaEventRecord(p->ev_busy, s));
+  return JT_OK;
+}
+
+// Phase marks for jt_last_profile: 0 call start, 1 call end, 2 + 2 i / 3 + 2 i axis i pass start / end,
+// 8 / 9 exchange start / end (comm stream).
+enum { PM_START = 0, PM_END = 1, PM_AX = 2, PM_XS = 8, PM_XE = 9 };
+jt_status mark(const jt_plan_s *p, int id, cudaStream_t s) {
+  if (!p->prof_on) return JT_OK;
+  if (!p->pev[id]) JT_CUDA_TRY(cudaEventCreate(&p->pev[id]));
+  JT_CUDA_TRY(cudaEventRecord(p->pev[id], s));
+  p->prec[id] = true;
+  return JT_OK;
+}
+void reset_marks(const jt_plan_s *p) {
+  for (auto &r : p->prec) r = false;
 }
 
 // Comm stream and events of the pipelined all-to-all (created on first use).
@@ -449,21 +574,53 @@ jt_status ensure_comm_stream(const jt_plan_s *p) {
   return JT_OK;
 }
 
+// In-process exchange of a virtual group (test only, include/jt_debug.h): rank `me` copies rows [off, off + cnt)
+// of block `me` of every member's send buffer into block g of its own receive buffer.  Barrier 1: every member
+// has published its send buffer and recorded "my rows are written" (ev_ready) on its stream; barrier 2: every
+// member has enqueued its copies and recorded "I have read my peers' rows" (ev_done); every stream then waits
+// for all ev_done, so no member reuses its send buffer before its peers' copies ran (NCCL's completion rule);
+// barrier 3: all those waits are enqueued before any member re-records its events in the next exchange.
+jt_status vgroup_exchange(const jt_plan_s *p, const double *send, double *recv, size_t chunk, size_t off, size_t cnt,
+                          cudaStream_t s) {
+  jt_vgroup_s *V = p->vgroup;
+  const int me = p->rank;
+  {
+    std::lock_guard<std::mutex> lk(V->mu);
+    V->send[me] = send;
+  }
+  JT_CUDA_TRY(cudaEventRecord(V->ev_ready[me], s));
+  if (!V->barrier()) return mark_broken(p, "virtual exchange: a peer did not arrive (barrier 1 timed out)");
+  for (int g = 0; g < V->G; ++g) {
+    JT_CUDA_TRY(cudaStreamWaitEvent(s, V->ev_ready[g], 0));
+    JT_CUDA_TRY(cudaMemcpyAsync(recv + g * chunk + off, V->send[g] + me * chunk + off, cnt * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+  }
+  JT_CUDA_TRY(cudaEventRecord(V->ev_done[me], s));
+  if (!V->barrier()) return mark_broken(p, "virtual exchange: a peer did not arrive (barrier 2 timed out)");
+  for (int g = 0; g < V->G; ++g) JT_CUDA_TRY(cudaStreamWaitEvent(s, V->ev_done[g], 0));
+  if (!V->barrier()) return mark_broken(p, "virtual exchange: a peer did not arrive (barrier 3 timed out)");
+  return JT_OK;
+}
+
 // All-to-all of rows [r0, r1) (rowlen elements each) of every contiguous chunk-major block (block g to /
-// from rank g) on stream s; the whole exchange is r0 = 0, r1 = rows per block.
-jt_status all_to_all_rows(const jt_plan_s *p, long long r0, long long r1, long long rowlen, cudaStream_t s) {
-  nccl::Api &A = nccl::api();
+// from rank g) between `send` and `recv` on stream s; the whole exchange is r0 = 0, r1 = rows per block.
+// A failure after earlier chunks were posted aborts the communicator (mark_broken), so the peers' pending
+// receives fail instead of hanging.
+jt_status all_to_all_rows(const jt_plan_s *p, const double *send, double *recv, long long r0, long long r1,
+                          long long rowlen, cudaStream_t s) {
   const size_t chunk = (size_t)p->total / p->nranks;
   const size_t off = (size_t)(r0 * rowlen), cnt = (size_t)((r1 - r0) * rowlen);
+  if (p->vgroup) return vgroup_exchange(p, send, recv, chunk, off, cnt, s);
+  nccl::Api &A = nccl::api();
   int e = A.GroupStart();
   for (int g = 0; g < p->nranks && e == nccl::Success; ++g) {
-    e = A.Send(p->a2a_send + g * chunk + off, cnt, nccl::Float64, g, p->comm, s);
-    if (e == nccl::Success) e = A.Recv(p->a2a_recv + g * chunk + off, cnt, nccl::Float64, g, p->comm, s);
+    e = A.Send(send + g * chunk + off, cnt, nccl::Float64, g, p->comm, s);
+    if (e == nccl::Success) e = A.Recv(recv + g * chunk + off, cnt, nccl::Float64, g, p->comm, s);
   }
   const int e2 = A.GroupEnd();
   if (e != nccl::Success || e2 != nccl::Success)
-    return fail(JT_ERR_NCCL, std::string("all-to-all: ") + A.GetErrorString(e != nccl::Success ? e : e2));
-  return JT_OK;
+    return mark_broken(p, std::string("all-to-all: ") + A.GetErrorString(e != nccl::Success ? e : e2));
+  return poll_comm(p);
 }
 
 // Slab schedule of a distributed plan (the C twin of paper_1901_07275_b200/dist.py SlabPlan):
@@ -472,80 +629,135 @@ jt_status all_to_all_rows(const jt_plan_s *p, long long r0, long long r1, long l
 //            sent (comm stream) while chunk k+1's axis-1 pass computes;
 //   inverse: axis d-1 and axis 0 (written chunk-major) on the y-slab, all-to-all, axis 1 read chunk-major; the
 //            all-to-all and the axis-1 pass are pipelined over KA row chunks of the x-slab (receiver side).
+//
+// JT_DIST_LOWMEM (NEXT-2 capacity mode): no plan-owned slab buffers; the caller's INPUT slab is the workspace
+// (its contents are destroyed) and the exchange runs between the caller's two slabs, not pipelined:
+//   forward: axis d-1 in place on `in`, axis 1 in -> out (chunk-major), all-to-all out -> in, axis 0 in -> out;
+//   inverse: axis d-1 in place on `in`, axis 0 in -> out (chunk-major), all-to-all out -> in, axis 1 in -> out.
 jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   const int G = p->nranks, d = p->d;
   const long long n0 = p->n[0], n1 = p->n[1], r = d == 3 ? p->n[2] : 1;
+  const long long R = n0 / G, c = n1 / G;  // slab rows, chunk length of axis 1
   jt_status st;
+  if ((st = ensure_comm_stream(p)) != JT_OK) return st;
+  if (p->dist_flags & JT_DIST_LOWMEM) {
+    double *work = const_cast<double *>(in);  // documented: the input slab is the workspace
+    if (d == 3) {
+      if ((st = mark(p, PM_AX + 4, s)) != JT_OK) return st;
+      if ((st = launch_axis(p, 2, inverse, work, work, inverse ? n0 * c : R * n1, 1, s)) != JT_OK) return st;
+      if ((st = mark(p, PM_AX + 5, s)) != JT_OK) return st;
+    }
+    const int ax1 = inverse ? 0 : 1;  // the pass before the exchange
+    if ((st = mark(p, PM_AX + 2 * ax1, s)) != JT_OK) return st;
+    if (inverse) st = launch_axis(p, 0, true, work, out, 1, c * r, s, 1, G);
+    else st = launch_axis(p, 1, false, work, out, R, r, s, 1, G);
+    if (st != JT_OK) return st;
+    if ((st = mark(p, PM_AX + 2 * ax1 + 1, s)) != JT_OK) return st;
+    if ((st = mark(p, PM_XS, s)) != JT_OK) return st;
+    if ((st = all_to_all_rows(p, out, work, 0, R, c * r, s)) != JT_OK) return st;
+    if ((st = mark(p, PM_XE, s)) != JT_OK) return st;
+    const int ax2 = inverse ? 1 : 0;
+    if ((st = mark(p, PM_AX + 2 * ax2, s)) != JT_OK) return st;
+    if (inverse) st = launch_axis(p, 1, true, work, out, R, r, s, G, 1);
+    else st = launch_axis(p, 0, false, work, out, 1, c * r, s);
+    if (st != JT_OK) return st;
+    return mark(p, PM_AX + 2 * ax2 + 1, s);
+  }
   if (!inverse) {
-    const long long R = n0 / G, c = n1 / G;  // slab rows, chunk length of axis 1
     const double *src1 = in;
     if (d == 3) {
+      if ((st = mark(p, PM_AX + 4, s)) != JT_OK) return st;
       if ((st = launch_axis(p, 2, false, in, out, R * n1, 1, s)) != JT_OK) return st;
+      if ((st = mark(p, PM_AX + 5, s)) != JT_OK) return st;
       src1 = out;
     }
-    if ((st = ensure_comm_stream(p)) != JT_OK) return st;
     const int KA = (int)std::min<long long>(4, R);  // (also at G = 1: the self-exchange path is exercised)
+    if ((st = mark(p, PM_AX + 2, s)) != JT_OK) return st;
     for (int k = 0; k < KA; ++k) {
       const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
       if (r1 == r0) continue;
       // rows [r0, r1) of the slab: input rows r0.., output rows r0.. of every chunk-major block
       if ((st = launch_axis(p, 1, false, src1 + r0 * n1 * r, p->a2a_send + r0 * c * r, r1 - r0, r, s, 1, G, -1, true,
-                            R)) != JT_OK)
+                            R, p->total - r0 * n1 * r, p->total - r0 * c * r)) != JT_OK)
         return st;
       JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], s));
       JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_chunk[k], 0));
-      if ((st = all_to_all_rows(p, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
+      if (k == 0 && (st = mark(p, PM_XS, p->s_comm)) != JT_OK) return st;
+      if ((st = all_to_all_rows(p, p->a2a_send, p->a2a_recv, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
     }
+    if ((st = mark(p, PM_AX + 3, s)) != JT_OK) return st;
+    if ((st = mark(p, PM_XE, p->s_comm)) != JT_OK) return st;
     JT_CUDA_TRY(cudaEventRecord(p->ev_comm, p->s_comm));
     JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
-    return launch_axis(p, 0, false, p->a2a_recv, out, 1, c * r, s);
+    if ((st = mark(p, PM_AX + 0, s)) != JT_OK) return st;
+    if ((st = launch_axis(p, 0, false, p->a2a_recv, out, 1, c * r, s)) != JT_OK) return st;
+    return mark(p, PM_AX + 1, s);
   }
-  const long long R = n0 / G, c = n1 / G;
   if (d == 3) {
+    if ((st = mark(p, PM_AX + 4, s)) != JT_OK) return st;
     if ((st = launch_axis(p, 2, true, in, out, n0 * c, 1, s)) != JT_OK) return st;
-    if ((st = launch_axis(p, 0, true, out, p->a2a_send, 1, c * r, s, 1, G)) != JT_OK) return st;
-  } else if ((st = launch_axis(p, 0, true, in, p->a2a_send, 1, c, s, 1, G)) != JT_OK) {
-    return st;
+    if ((st = mark(p, PM_AX + 5, s)) != JT_OK) return st;
   }
-  if ((st = ensure_comm_stream(p)) != JT_OK) return st;
+  if ((st = mark(p, PM_AX + 0, s)) != JT_OK) return st;
+  if ((st = launch_axis(p, 0, true, d == 3 ? out : in, p->a2a_send, 1, c * r, s, 1, G)) != JT_OK) return st;
+  if ((st = mark(p, PM_AX + 1, s)) != JT_OK) return st;
   JT_CUDA_TRY(cudaEventRecord(p->ev_comm, s));
   JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_comm, 0));
   // the exchange in KA row chunks of the x-slab on the comm stream; chunk k's axis-1 pass waits for its rows only
   const int KA = (int)std::min<long long>(4, R);
+  if ((st = mark(p, PM_XS, p->s_comm)) != JT_OK) return st;
+  bool first = true;
   for (int k = 0; k < KA; ++k) {
     const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
     if (r1 == r0) continue;
-    if ((st = all_to_all_rows(p, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
+    if ((st = all_to_all_rows(p, p->a2a_send, p->a2a_recv, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
     JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], p->s_comm));
     JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_chunk[k], 0));
+    if (first && (st = mark(p, PM_AX + 2, s)) != JT_OK) return st;
+    first = false;
     if ((st = launch_axis(p, 1, true, p->a2a_recv + r0 * c * r, out + r0 * n1 * r, r1 - r0, r, s, G, 1, -1, true,
-                          R)) != JT_OK)
+                          R, p->total - r0 * c * r, p->total - r0 * n1 * r)) != JT_OK)
       return st;
+  }
+  if ((st = mark(p, PM_XE, p->s_comm)) != JT_OK) return st;
+  // the comm stream's last use of the plan's buffers is ordered before the call's end (ev_busy on s)
+  JT_CUDA_TRY(cudaEventRecord(p->ev_comm, p->s_comm));
+  JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
+  return mark(p, PM_AX + 3, s);
+}
+
+// Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
+jt_status transform_body(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
+  jt_status st;
+  if (p->dist) return transform_dist(p, inverse, in, out, s);
+  const double *src = in;
+  for (int axis = p->d - 1; axis >= 0; --axis) {
+    long long outer = 1, inner = 1;
+    for (int i = 0; i < axis; ++i) outer *= p->n[i];
+    for (int i = axis + 1; i < p->d; ++i) inner *= p->n[i];
+    if ((st = mark(p, PM_AX + 2 * axis, s)) != JT_OK) return st;
+    if ((st = launch_axis(p, axis, inverse, src, out, outer, inner, s)) != JT_OK) return st;
+    if ((st = mark(p, PM_AX + 2 * axis + 1, s)) != JT_OK) return st;
+    src = out;
   }
   return JT_OK;
 }
 
-// Axis schedule: axis d-1 (contiguous) first, reading `in`, then axes d-2..0 in place on `out`.
 jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   jt_status st = check_device_plan(p);
   p->launches = 0;
   if (st != JT_OK) return st;
   if (!in || !out) return fail(JT_ERR_ARG, "null data pointer");
   if (overlaps_partially(in, out, p->total)) return fail(JT_ERR_ARG, "input and output partially overlap");
+  if (p->dist && in == out)
+    return fail(JT_ERR_ARG, "distributed transforms are out of place (x-slab and y-slab differ)");
   DeviceGuard g(p->device);
-  if (p->dist) {
-    if (in == out) return fail(JT_ERR_ARG, "distributed transforms are out of place (x-slab and y-slab differ)");
-    return transform_dist(p, inverse, in, out, s);
-  }
-  const double *src = in;
-  for (int axis = p->d - 1; axis >= 0; --axis) {
-    long long outer = 1, inner = 1;
-    for (int i = 0; i < axis; ++i) outer *= p->n[i];
-    for (int i = axis + 1; i < p->d; ++i) inner *= p->n[i];
-    if ((st = launch_axis(p, axis, inverse, src, out, outer, inner, s)) != JT_OK) return st;
-    src = out;
-  }
-  return JT_OK;
+  reset_marks(p);
+  if ((st = begin_call(p, s)) != JT_OK) return st;
+  if ((st = mark(p, PM_START, s)) != JT_OK) return st;
+  if ((st = transform_body(p, inverse, in, out, s)) != JT_OK) return st;
+  if ((st = mark(p, PM_END, s)) != JT_OK) return st;
+  return end_call(p, s);
 }
 
 // Host-buffer transform, pipelined (DESIGN.md §10 "e2e"): the input is copied in KC row chunks of axis 0
@@ -553,12 +765,29 @@ jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *
 // chunk); the axis-0 pass then runs in KC column blocks, each copied back (a pitched 2D copy) on a second
 // copy stream while the next block computes.  Every line runs the same kernel code as in jt_forward /
 // jt_inverse, so the results equal the device path's up to rounding (term-split launches sum in another order).
+// Wait for stream s; on a distributed plan poll the communicator meanwhile, so a failed peer surfaces as
+// JT_ERR_NCCL (and aborts the communicator) instead of a hang.
+jt_status wait_stream(const jt_plan_s *p, cudaStream_t s) {
+  if (!p->dist || !p->comm) {
+    JT_CUDA_TRY(cudaStreamSynchronize(s));
+    return JT_OK;
+  }
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return JT_OK;
+    if (e != cudaErrorNotReady) return fail(JT_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+    jt_status st = poll_comm(p);
+    if (st != JT_OK) return st;
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 jt_status host_wait(jt_plan_s *p) {
   if (!p->s_d2h) return JT_OK;
   DeviceGuard g(p->device);
-  JT_CUDA_TRY(cudaStreamSynchronize(p->s_h2d));
-  JT_CUDA_TRY(cudaStreamSynchronize(p->s_d2h));
-  return JT_OK;
+  jt_status st = wait_stream(p, p->s_h2d);
+  if (st != JT_OK) return st;
+  return wait_stream(p, p->s_d2h);
 }
 
 jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double *out_h, cudaStream_t s,
@@ -575,7 +804,9 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     for (auto &e : p->ev) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : p->ev_free) JT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  const int slot = (int)(p->host_calls++ % JT_HOST_SLOTS);
+  // (JT_DIST_LOWMEM: one staging slot, i.e. the two slabs of the capacity mode, and no pipelining)
+  const bool lowmem = p->dist && (p->dist_flags & JT_DIST_LOWMEM);
+  const int slot = lowmem ? 0 : (int)(p->host_calls++ % JT_HOST_SLOTS);
   if (!p->stage_in[slot]) {
     if (cudaMalloc((void **)&p->stage_in[slot], bytes) != cudaSuccess ||
         cudaMalloc((void **)&p->stage_out[slot], bytes) != cudaSuccess)
@@ -584,13 +815,16 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
   }
   double *sin = p->stage_in[slot], *sout = p->stage_out[slot];
   cudaEvent_t *ev_in = p->ev, *ev_out = p->ev + 16, ev_start = p->ev[32];
-  // ordering: the caller's prior work on s first; the slot's previous use (its output copy) finished
+  // ordering: the caller's prior work on s first; the slot's previous use (its output copy) finished; the
+  // previous call's use of the plan's other buffers (all-to-all, term-split workspace) finished
+  reset_marks(p);
+  if ((st = begin_call(p, s)) != JT_OK) return st;
   JT_CUDA_TRY(cudaEventRecord(ev_start, s));
   JT_CUDA_TRY(cudaStreamWaitEvent(p->s_h2d, p->ev_free[slot], 0));
   JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_free[slot], 0));
   JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_start, 0));
   const int d = p->d;
-  if (p->dist && !inverse) {
+  if (p->dist && !inverse && !lowmem) {
     // distributed forward (transform_dist's schedule, pipelined with the copies): the x-slab arrives in KA row
     // chunks; each chunk's axes d-1..1 and its rows of the all-to-all run as soon as it is in; the axis-0 pass on
     // the received y-slab runs in column blocks, each copied back (pitched) while the next computes
@@ -608,14 +842,17 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
       JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[k], 0));
       const double *src1 = sin + off;
       if (d == 3) {
-        if ((st = launch_axis(p, 2, false, sin + off, sout + off, (r1 - r0) * n1, 1, s)) != JT_OK) return st;
+        if ((st = launch_axis(p, 2, false, sin + off, sout + off, (r1 - r0) * n1, 1, s, 1, 1, -1, true, -1,
+                              p->total - (long long)off, p->total - (long long)off)) != JT_OK)
+          return st;
         src1 = sout + off;
       }
-      if ((st = launch_axis(p, 1, false, src1, p->a2a_send + r0 * c * r, r1 - r0, r, s, 1, G, -1, true, R)) != JT_OK)
+      if ((st = launch_axis(p, 1, false, src1, p->a2a_send + r0 * c * r, r1 - r0, r, s, 1, G, -1, true, R,
+                            p->total - (long long)off, p->total - r0 * c * r)) != JT_OK)
         return st;
       JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], s));
       JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_chunk[k], 0));
-      if ((st = all_to_all_rows(p, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
+      if ((st = all_to_all_rows(p, p->a2a_send, p->a2a_recv, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
     }
     JT_CUDA_TRY(cudaEventRecord(p->ev_comm, p->s_comm));
     JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
@@ -623,18 +860,20 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     for (int cb = 0; cb < KC; ++cb) {
       const long long c0 = yrow * cb / KC, c1 = yrow * (cb + 1) / KC;
       if (c1 == c0) continue;
-      if ((st = launch_axis(p, 0, false, p->a2a_recv + c0, sout + c0, 1, yrow, s, 1, 1, c1 - c0)) != JT_OK) return st;
+      if ((st = launch_axis(p, 0, false, p->a2a_recv + c0, sout + c0, 1, yrow, s, 1, 1, c1 - c0, true, -1,
+                            p->total - c0, p->total - c0)) != JT_OK)
+        return st;
       JT_CUDA_TRY(cudaEventRecord(ev_out[cb], s));
       JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[cb], 0));
       JT_CUDA_TRY(cudaMemcpy2DAsync(out_h + c0, (size_t)yrow * sizeof(double), sout + c0, (size_t)yrow * sizeof(double),
                                     (size_t)(c1 - c0) * sizeof(double), (size_t)n0, cudaMemcpyDeviceToHost,
                                     p->s_d2h));
     }
-  } else if (p->dist || d == 1) {  // distributed inverse / one line: copy in, transform, copy out
+  } else if (p->dist || d == 1) {  // distributed inverse (or capacity mode) / one line: copy in, transform, copy out
     JT_CUDA_TRY(cudaMemcpyAsync(sin, in_h, bytes, cudaMemcpyHostToDevice, p->s_h2d));
     JT_CUDA_TRY(cudaEventRecord(ev_in[0], p->s_h2d));
     JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[0], 0));
-    if ((st = transform(p, inverse, sin, sout, s)) != JT_OK) return st;
+    if ((st = transform_body(p, inverse, sin, sout, s)) != JT_OK) return st;
     JT_CUDA_TRY(cudaEventRecord(ev_out[0], s));
     JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[0], 0));
     JT_CUDA_TRY(cudaMemcpyAsync(out_h, sout, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
@@ -654,7 +893,9 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
         long long outer = r1 - r0, inner = 1;
         for (int i = 1; i < axis; ++i) outer *= p->n[i];
         for (int i = axis + 1; i < d; ++i) inner *= p->n[i];
-        if ((st = launch_axis(p, axis, inverse, src, sout + off, outer, inner, s)) != JT_OK) return st;
+        if ((st = launch_axis(p, axis, inverse, src, sout + off, outer, inner, s, 1, 1, -1, true, -1,
+                              p->total - (long long)off, p->total - (long long)off)) != JT_OK)
+          return st;
         src = sout + off;
       }
     }
@@ -662,7 +903,9 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     for (int c = 0; c < KC; ++c) {
       const long long c0 = row * c / KC, c1 = row * (c + 1) / KC;
       if (c1 == c0) continue;
-      if ((st = launch_axis(p, 0, inverse, sout + c0, sout + c0, 1, row, s, 1, 1, c1 - c0)) != JT_OK) return st;
+      if ((st = launch_axis(p, 0, inverse, sout + c0, sout + c0, 1, row, s, 1, 1, c1 - c0, true, -1, p->total - c0,
+                            p->total - c0)) != JT_OK)
+        return st;
       JT_CUDA_TRY(cudaEventRecord(ev_out[c], s));
       JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[c], 0));
       JT_CUDA_TRY(cudaMemcpy2DAsync(out_h + c0, (size_t)row * sizeof(double), sout + c0, (size_t)row * sizeof(double),
@@ -671,6 +914,7 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     }
   }
   JT_CUDA_TRY(cudaEventRecord(p->ev_free[slot], p->s_d2h));
+  if ((st = end_call(p, s)) != JT_OK) return st;
   return wait ? host_wait(p) : JT_OK;
 }
 
@@ -865,8 +1109,11 @@ static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *i
     return fail(JT_ERR_ARG, "chunk-major layouts need out-of-place buffers");
   DeviceGuard g(p->device);
   if (ostride >= 0 && ostride < outer) return fail(JT_ERR_ARG, "ostride must be >= outer");
-  return launch_axis(p, axis, inverse, in, out, outer, inner, (cudaStream_t)stream, in_split, out_split, -1, true,
-                     ostride);
+  const cudaStream_t s = (cudaStream_t)stream;
+  if ((st = begin_call(p, s)) != JT_OK) return st;
+  if ((st = launch_axis(p, axis, inverse, in, out, outer, inner, s, in_split, out_split, -1, true, ostride)) != JT_OK)
+    return st;
+  return end_call(p, s);
 }
 
 jt_status jt_forward_axis(jt_plan_t p, int axis, const double *in, double *out, int64_t outer, int64_t inner,
@@ -900,41 +1147,173 @@ jt_status jt_dist_unique_id(void *nccl_unique_id) {
   return JT_OK;
 }
 
-jt_status jt_plan_dist(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
-                       const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks) {
+// Shared by jt_plan_dist_ex (NCCL communicator) and jt_debug_plan_virtual (in-process group).
+static jt_status plan_dist_common(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
+                                  double eps, const jt_opts *opts, int rank, int nranks, int flags,
+                                  const void *nccl_unique_id, jt_vgroup_t group) {
   if (!out) return fail(JT_ERR_ARG, "null out");
   *out = nullptr;
   if (d != 2 && d != 3) return fail(JT_ERR_ARG, "distributed plans need d = 2 or 3");
-  if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return fail(JT_ERR_ARG, "bad rank / nranks / id");
+  if ((!nccl_unique_id && !group) || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(JT_ERR_ARG, "bad rank / nranks / id");
+  if (flags & ~JT_DIST_LOWMEM) return fail(JT_ERR_ARG, "unknown JT_DIST_* flag");
   if (!n || n[0] % nranks != 0 || n[1] % nranks != 0)
     return fail(JT_ERR_ARG, "n[0] and n[1] must be divisible by nranks");
   if (opts && opts->device == -2) return fail(JT_ERR_ARG, "distributed plans need a device");
   nccl::Api &A = nccl::api();
-  if (!A.ok) return fail(JT_ERR_NCCL, A.why);
+  if (!group && !A.ok) return fail(JT_ERR_NCCL, A.why);
   jt_plan_t p = nullptr;
   jt_status st = jt_plan(&p, d, n, a, b, eps, opts);
   if (st != JT_OK) return st;
   p->dist = true;
   p->rank = rank;
   p->nranks = nranks;
+  p->dist_flags = flags;
   p->total /= nranks;  // local slab elements
   DeviceGuard g(p->device);
-  nccl::UniqueId id;
-  std::memcpy(&id, nccl_unique_id, sizeof(id));
-  const int e = A.CommInitRank(&p->comm, nranks, id, rank);
-  if (e != nccl::Success) {
-    std::string msg = std::string("ncclCommInitRank: ") + A.GetErrorString(e);
-    p->comm = nullptr;
-    jt_destroy(p);
-    return fail(JT_ERR_NCCL, msg);
+  if (group) {
+    std::lock_guard<std::mutex> lk(group->mu);
+    if (group->member[rank]) {
+      jt_destroy(p);
+      return fail(JT_ERR_ARG, "virtual group: rank already has a plan");
+    }
+    if (cudaEventCreateWithFlags(&group->ev_ready[rank], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&group->ev_done[rank], cudaEventDisableTiming) != cudaSuccess) {
+      jt_destroy(p);
+      return fail(JT_ERR_CUDA, "virtual group events");
+    }
+    group->member[rank] = p;
+    p->vgroup = group;
+  } else {
+    nccl::UniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    const int e = A.CommInitRank(&p->comm, nranks, id, rank);
+    if (e != nccl::Success) {
+      std::string msg = std::string("ncclCommInitRank: ") + A.GetErrorString(e);
+      p->comm = nullptr;
+      jt_destroy(p);
+      return fail(JT_ERR_NCCL, msg);
+    }
   }
-  const size_t bytes = (size_t)p->total * sizeof(double);
-  if (cudaMalloc((void **)&p->a2a_send, bytes) != cudaSuccess || cudaMalloc((void **)&p->a2a_recv, bytes) != cudaSuccess) {
-    jt_destroy(p);
-    return fail(JT_ERR_ALLOC, "all-to-all buffers");
+  if (!(flags & JT_DIST_LOWMEM)) {
+    const size_t bytes = (size_t)p->total * sizeof(double);
+    if (cudaMalloc((void **)&p->a2a_send, bytes) != cudaSuccess ||
+        cudaMalloc((void **)&p->a2a_recv, bytes) != cudaSuccess) {
+      jt_destroy(p);
+      return fail(JT_ERR_ALLOC, "all-to-all buffers");
+    }
   }
   *out = p;
   return JT_OK;
+}
+
+jt_status jt_plan_dist(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
+                       const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks) {
+  return plan_dist_common(out, d, n, a, b, eps, opts, rank, nranks, 0, nccl_unique_id, nullptr);
+}
+
+jt_status jt_plan_dist_ex(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
+                          const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks, int flags) {
+  if (!nccl_unique_id) return fail(JT_ERR_ARG, "null id");
+  return plan_dist_common(out, d, n, a, b, eps, opts, rank, nranks, flags, nccl_unique_id, nullptr);
+}
+
+jt_status jt_sync(jt_plan_t p, void *cuda_stream) {
+  if (!p) return fail(JT_ERR_ARG, "null plan");
+  if (p->device < 0) return fail(JT_ERR_ARG, "host-only plan");
+  DeviceGuard g(p->device);
+  jt_status st = p->dist ? poll_comm(p) : JT_OK;
+  if (st != JT_OK) return st;
+  return wait_stream(p, (cudaStream_t)cuda_stream);
+}
+
+jt_status jt_profile(jt_plan_t p, int enable) {
+  if (!p) return fail(JT_ERR_ARG, "null plan");
+  p->prof_on = enable != 0;
+  reset_marks(p);
+  return JT_OK;
+}
+
+jt_status jt_last_profile(jt_plan_t p, double ms[5]) {
+  if (!p || !ms) return fail(JT_ERR_ARG, "null argument");
+  if (!p->prof_on || !p->prec[PM_START] || !p->prec[PM_END])
+    return fail(JT_ERR_ARG, "no profiled call (jt_profile(p, 1) before a jt_forward / jt_inverse)");
+  DeviceGuard g(p->device);
+  auto span = [&](int a, int b) -> double {
+    if (!p->prec[a] || !p->prec[b]) return 0.0;
+    float t = 0;
+    if (cudaEventSynchronize(p->pev[b]) != cudaSuccess || cudaEventElapsedTime(&t, p->pev[a], p->pev[b]) != cudaSuccess)
+      return -1.0;
+    return (double)t;
+  };
+  for (int i = 0; i < 3; ++i) ms[i] = span(PM_AX + 2 * i, PM_AX + 2 * i + 1);
+  ms[3] = span(PM_XS, PM_XE);
+  ms[4] = span(PM_START, PM_END);
+  for (int i = 0; i < 5; ++i)
+    if (ms[i] < 0) return fail(JT_ERR_CUDA, "profile events");
+  return JT_OK;
+}
+
+// ---- test hooks (include/jt_debug.h) ----
+jt_status jt_debug_axis_pass_lim(jt_plan_t p, int axis, int inverse, const double *in, double *out, int64_t outer,
+                                 int64_t inner, int64_t in_lim, int64_t out_lim, void *stream) {
+  jt_status st = check_device_plan(p);
+  if (st != JT_OK) return st;
+  if (axis < 0 || axis >= p->d || !in || !out || outer < 1 || inner < 1 || in_lim < 0 || out_lim < 0)
+    return fail(JT_ERR_ARG, "bad args");
+  p->launches = 0;
+  DeviceGuard g(p->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  if ((st = begin_call(p, s)) != JT_OK) return st;
+  // (no term split: the reduction kernel writes the output without the kernels' checks)
+  if ((st = launch_axis(p, axis, inverse != 0, in, out, outer, inner, s, 1, 1, -1, false, -1, in_lim, out_lim)) != JT_OK)
+    return st;
+  return end_call(p, s);
+}
+
+jt_status jt_debug_checks(int *enabled, unsigned long long *count, int *line) {
+  if (!enabled || !count || !line) return fail(JT_ERR_ARG, "null argument");
+  *enabled = JT_CHECKS;
+  unsigned long long c = 0;
+  int l = 0;
+  JT_CUDA_TRY(cudaDeviceSynchronize());
+  JT_CUDA_TRY(cudaMemcpyFromSymbol(&c, jtk::jt_check_count, sizeof(c)));
+  JT_CUDA_TRY(cudaMemcpyFromSymbol(&l, jtk::jt_check_line, sizeof(l)));
+  *count = c;
+  *line = l;
+  const unsigned long long z = 0;
+  const int zl = 0;
+  JT_CUDA_TRY(cudaMemcpyToSymbol(jtk::jt_check_count, &z, sizeof(z)));
+  JT_CUDA_TRY(cudaMemcpyToSymbol(jtk::jt_check_line, &zl, sizeof(zl)));
+  return JT_OK;
+}
+
+jt_status jt_debug_vgroup_create(jt_vgroup_t *out, int nranks, int timeout_ms) {
+  if (!out || nranks < 1 || timeout_ms < 1) return fail(JT_ERR_ARG, "bad args");
+  jt_vgroup_s *V = new (std::nothrow) jt_vgroup_s();
+  if (!V) return fail(JT_ERR_ALLOC, "group");
+  V->G = nranks;
+  V->timeout_ms = timeout_ms;
+  V->member.assign(nranks, nullptr);
+  V->send.assign(nranks, nullptr);
+  V->ev_ready.assign(nranks, nullptr);
+  V->ev_done.assign(nranks, nullptr);
+  *out = V;
+  return JT_OK;
+}
+
+jt_status jt_debug_vgroup_destroy(jt_vgroup_t g) {
+  if (!g) return JT_OK;
+  for (jt_plan_s *m : g->member)
+    if (m) return fail(JT_ERR_ARG, "virtual group still has plans: destroy them first");
+  delete g;
+  return JT_OK;
+}
+
+jt_status jt_debug_plan_virtual(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
+                                double eps, const jt_opts *opts, jt_vgroup_t group, int rank, int flags) {
+  if (!group) return fail(JT_ERR_ARG, "null group");
+  return plan_dist_common(out, d, n, a, b, eps, opts, rank, group->G, flags, nullptr, group);
 }
 
 jt_status jt_local_box(jt_plan_t p, int which, int64_t lo[], int64_t hi[]) {

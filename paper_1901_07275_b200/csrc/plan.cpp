@@ -100,52 +100,50 @@ static void pn_eval(const Recurrence &R, int64_t n, ld t, ld &pn, ld &dpn, ld &k
   ksum = s;
 }
 
-// Eigenvalues of the symmetric tridiagonal matrix (diag d, off-diagonal e[i] between i and i+1)
-// by the implicit QL algorithm with Wilkinson-type shifts (eigenvalues only, O(n^2)).
+// Eigenvalues of the symmetric tridiagonal matrix T (diagonal d[0..n-1], off-diagonal e[k] = T[k][k+1])
+// by implicit symmetric QR steps with the Wilkinson shift (the textbook method, e.g. Golub & Van Loan,
+// "Matrix Computations", symmetric tridiagonal QR): the bottom of the active range shrinks whenever its last
+// off-diagonal is negligible; otherwise one shifted step runs on the unreduced block [lo, hi] ending there.
+// The step starts with the plane rotation that maps the first column (d[lo] - mu, e[lo]) of T - mu I onto a
+// multiple of e_lo, applies it as a similarity, and chases the resulting bulge (the entry T[k-1][k+1])
+// down the diagonal with one rotation per row.  Eigenvalues only, O(n^2) overall; the nodes are polished by
+// Newton afterwards, so this only has to land each eigenvalue in its root's basin.
 static bool tridiag_eigenvalues(std::vector<ld> &d, std::vector<ld> e) {
   const int64_t n = (int64_t)d.size();
-  e.resize(n, 0);
-  if (n > 0) e[n - 1] = 0;
-  for (int64_t l = 0; l < n; ++l) {
-    int iter = 0;
-    int64_t m;
-    do {
-      for (m = l; m < n - 1; ++m) {
-        ld dd = fabsl(d[m]) + fabsl(d[m + 1]);
-        if (fabsl(e[m]) <= LDBL_EPSILON * dd) break;
+  if (n <= 1) return true;
+  e.resize(n - 1);
+  auto negligible = [&](int64_t k) { return fabsl(e[k]) <= LDBL_EPSILON * (fabsl(d[k]) + fabsl(d[k + 1])); };
+  int64_t hi = n - 1;
+  int64_t steps = 0;
+  while (hi > 0) {
+    if (negligible(hi - 1)) {  // T[hi][hi] has decoupled: it is an eigenvalue
+      e[hi - 1] = 0;
+      --hi;
+      continue;
+    }
+    if (++steps > 40 * n) return false;
+    int64_t lo = hi - 1;
+    while (lo > 0 && !negligible(lo - 1)) --lo;
+    // Wilkinson shift: the eigenvalue of the trailing 2x2 block closer to its last diagonal entry
+    const ld half = (d[hi - 1] - d[hi]) / 2, off = e[hi - 1];
+    const ld root = hypotl(half, off);
+    const ld mu = d[hi] - off * off / (half + (half < 0 ? -root : root));
+    ld x = d[lo] - mu, z = e[lo];
+    for (int64_t k = lo; k < hi; ++k) {
+      // rotation [c s; -s c] in the plane (k, k+1) with [c s; -s c] (x, z)^T = (rho, 0)^T
+      const ld rho = hypotl(x, z);
+      const ld c = rho == 0 ? 1 : x / rho, s = rho == 0 ? 0 : z / rho;
+      if (k > lo) e[k - 1] = rho;  // the bulge T[k-1][k+1] is gone
+      const ld dk = d[k], dk1 = d[k + 1], ek = e[k];
+      d[k] = c * c * dk + 2 * c * s * ek + s * s * dk1;
+      d[k + 1] = s * s * dk - 2 * c * s * ek + c * c * dk1;
+      e[k] = c * s * (dk1 - dk) + (c * c - s * s) * ek;
+      if (k + 1 < hi) {  // the rotation of row k+1 pushes part of e[k+1] into the new bulge T[k][k+2]
+        x = e[k];
+        z = s * e[k + 1];
+        e[k + 1] *= c;
       }
-      if (m != l) {
-        if (++iter > 60) return false;
-        ld g = (d[l + 1] - d[l]) / (2 * e[l]);
-        ld rr = hypotl(g, 1.0L);
-        g = d[m] - d[l] + e[l] / (g + copysignl(rr, g));
-        ld s = 1, c = 1, p = 0;
-        int64_t i;
-        bool underflow = false;
-        for (i = m - 1; i >= l; --i) {
-          ld f = s * e[i], bb = c * e[i];
-          rr = hypotl(f, g);
-          e[i + 1] = rr;
-          if (rr == 0) {
-            d[i + 1] -= p;
-            e[m] = 0;
-            underflow = true;
-            break;
-          }
-          s = f / rr;
-          c = g / rr;
-          g = d[i + 1] - p;
-          rr = (d[i] - g) * s + 2 * c * bb;
-          p = s * rr;
-          d[i + 1] = g + p;
-          g = c * rr - bb;
-        }
-        if (underflow) continue;
-        d[l] -= p;
-        e[l] = g;
-        e[m] = 0;
-      }
-    } while (m != l);
+    }
   }
   return true;
 }
@@ -684,6 +682,11 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
   int rmax = opts.rmax_init > 0 ? opts.rmax_init
                                 : std::max(32, (int)std::ceil(2 * std::log2((double)std::max<int64_t>(n, 2))));
   rmax = std::min(rmax, cap);
+  // Growth cap ("growth cap (r > min(m,n)/4) aborts"; reading R25): the doubling may
+  // raise rmax beyond its start value only up to min(n, n - k0) / 4; a factorisation still unconverged there
+  // is JT_ERR_NUMERIC (the factored form would no longer be cheaper than the dense product).  A start value at
+  // the full size (small n: B is factored exactly) never grows and never fails.
+  const int grow_cap = std::max(rmax, cap / 4);
   std::mt19937_64 rng(opts.seed ^ 0x9E3779B97F4A7C15ULL);
   CMat U0, V0h;
   std::vector<double> sig;
@@ -692,7 +695,12 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
     double s0 = sig.empty() ? 0 : sig[0];
     bool converged = sig.size() < (size_t)rmax || sig.back() <= 0.1 * eps * s0;
     if (converged || rmax >= cap) break;
-    rmax = std::min(cap, 2 * rmax);
+    if (rmax >= grow_cap) {
+      err = "adaptive rank exceeded its growth cap min(n, n-k0)/4 = " + std::to_string(cap / 4) +
+            " (rmax " + std::to_string(rmax) + " not converged at eps)";
+      return JT_ERR_NUMERIC;
+    }
+    rmax = std::min(grow_cap, 2 * rmax);
   }
   ax.rmax_used = rmax;
   ax.sigma = sig;

@@ -230,19 +230,30 @@ class LibSlabPlan:
     torch.distributed is only used to broadcast the 128-byte NCCL unique id from rank 0.  This is the path
     bench.py times; `SlabPlan` above is its host-side twin used by the gloo CPU tests."""
 
-    def __init__(self, shape, a, b, eps, dist, group=None, **plan_kw):
+    def __init__(self, shape, a, b, eps, dist=None, group=None, flags: int = 0, vgroup=None, rank=None,
+                 **plan_kw):
+        """dist/group: the torch.distributed module and process group (NCCL communicator created inside the
+        library).  Test mode (include/jt_debug.h): vgroup = a jt_debug_vgroup_create handle and rank = this
+        virtual rank, no torch.distributed (the library's in-process exchange instead of NCCL).
+        flags: JT_DIST_LOWMEM (capacity mode: the input slab is the workspace and is destroyed)."""
         import torch
-        from . import jt_destroy, jt_dist_unique_id, jt_local_box, jt_plan_dist, jt_plan_info, jt_plan_rank
+        from . import (jt_debug_plan_virtual, jt_destroy, jt_dist_unique_id, jt_local_box, jt_plan_dist,
+                       jt_plan_info, jt_plan_rank)
         self.shape = tuple(int(v) for v in shape)
         self.d = len(self.shape)
-        self.G = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if self.rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(jt_dist_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, src=0, group=group)
-        self.handle = jt_plan_dist(self.shape, a, b, eps, bytes(uid.cpu().numpy().tobytes()), self.rank, self.G,
-                                   **plan_kw)
+        self.flags = flags
+        if vgroup is not None:
+            self.rank = int(rank)
+            self.handle = jt_debug_plan_virtual(self.shape, a, b, eps, vgroup, self.rank, flags=flags, **plan_kw)
+        else:
+            self.G = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if self.rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(jt_dist_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, src=0, group=group)
+            self.handle = jt_plan_dist(self.shape, a, b, eps, bytes(uid.cpu().numpy().tobytes()), self.rank, self.G,
+                                       flags=flags, **plan_kw)
         self._destroy = jt_destroy
         self.ranks = [jt_plan_rank(self.handle, i) for i in range(self.d)]
         self.infos = [jt_plan_info(self.handle, i) for i in range(self.d)]
@@ -251,6 +262,7 @@ class LibSlabPlan:
         self.box = {0: (lo0, hi0), 1: (lo1, hi1)}
         self.x_shape = tuple(h - l for l, h in zip(lo0, hi0))
         self.y_shape = tuple(h - l for l, h in zip(lo1, hi1))
+        self.G = self.shape[0] // self.x_shape[0]
         self.device = torch.device("cuda", torch.cuda.current_device())
 
     def local_box(self, which: int):
@@ -266,25 +278,33 @@ class LibSlabPlan:
         lo, hi = self.box[1]
         return torch.as_tensor(full)[:, lo[1]:hi[1]].contiguous().to(self.device)
 
-    def forward(self, x, out=None):
+    def forward(self, x, out=None, stream=None):
+        """x-slab -> y-slab (with JT_DIST_LOWMEM the x-slab is overwritten: it is the workspace)."""
         import torch
         from . import jt_forward
         out = torch.empty(self.y_shape, dtype=torch.float64, device=self.device) if out is None else out
-        jt_forward(self.handle, x, out)
+        jt_forward(self.handle, x, out, stream)
         return out
 
-    def inverse(self, y, out=None):
+    def inverse(self, y, out=None, stream=None):
+        """y-slab -> x-slab (with JT_DIST_LOWMEM the y-slab is overwritten)."""
         import torch
         from . import jt_inverse
         out = torch.empty(self.x_shape, dtype=torch.float64, device=self.device) if out is None else out
-        jt_inverse(self.handle, y, out)
+        jt_inverse(self.handle, y, out, stream)
         return out
 
-    def forward_host(self, x_host, y_host, x_dev=None, y_dev=None):
+    def forward_host(self, x_host, y_host, x_dev=None, y_dev=None, stream=None):
         """End-to-end forward of this rank's slab from / to (pinned) host memory (C: jt_forward_host)."""
         from . import jt_forward_host
-        jt_forward_host(self.handle, x_host.numpy(), y_host.numpy())
+        jt_forward_host(self.handle, x_host.numpy(), y_host.numpy(), stream)
         return y_host
+
+    def inverse_host(self, y_host, x_host, stream=None):
+        """End-to-end inverse of this rank's y-slab (C: jt_inverse_host)."""
+        from . import jt_inverse_host
+        jt_inverse_host(self.handle, y_host.numpy(), x_host.numpy(), stream)
+        return x_host
 
     def forward_host_async(self, x_host, y_host, stream=None):
         """Enqueue an end-to-end forward of this rank's slab (C: jt_forward_host_async; consecutive calls overlap
