@@ -235,6 +235,13 @@ def main():
     dist = None
     if slab:
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # `--slab` without torchrun: a world of one over NCCL
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(port))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_1901_07275_b200.dist import LibSlabPlan
     shape, a, b, eps = cfg["n"], cfg["a"], cfg["b"], cfg["eps"]
