@@ -180,7 +180,8 @@ struct Cfg {
   static constexpr bool TPRIV = PRIV && JT_TPRIV && N <= JT_TPRIV_NMAX;
   // exchange one real plane at a time (3 group barriers per exchange) only while SMEM is short: with the state
   // in TMEM the full complex exchange (1 barrier) fits
-  static constexpr bool SPLITX = R >= 32 && (!TPRIV || JT_SPLITX_TPRIV);
+  // (SUB: the split exchange halves the exchange buffers, room for a ring deeper than one term)
+  static constexpr bool SPLITX = R >= 32 && (!TPRIV || JT_SPLITX_TPRIV || (N == 4096 && MAXR == 2 && JT_SUB && JT_SUB_SPLITX));
 
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
   // (MAXR = 4: twice the row accumulators / bin rows per thread)
@@ -202,13 +203,22 @@ struct Cfg {
   // next to the exchange buffers (URING), filled a whole term ahead of its use; v_l still through L1
 // (measured: N = 2048 forward -5 %; N = 4096 +8 %: its 64 KB stage leaves too little L1 for the v_l loads)
   static constexpr bool URING_WANT = !STAGED && !INV && JT_URING && N <= JT_URING_NMAX;
+  // N = 4096 (SUB): a term's factors (128 KB) do not fit a stage, so they stream through a ring of 16 KB SUB-stages
+  // shared by the CTA's groups, in the order the term consumes them -- forward: v_l in 4 blocks of 1024 positions
+  // (A1), then u~_l in 4 blocks of bins (A3); inverse: u~_l in 4 bin blocks (bin sums), then v_l in 4 blocks
+  // (accumulate) -- each released per WARP as soon as its values are in registers (no extra group barrier); the
+  // last warp to release a slot refills it NSTAGE sub-stages ahead.  Replaces the L1/L2 factor loads (the top
+  // stall of these passes, long-scoreboard, 40x the algorithmic bytes through L2).
+  static constexpr bool SUB = N == 4096 && R == 32 && MAXR == 2 && JT_SUB;
+  static constexpr int SUBB = 16384, NSUB = 8;  // bytes per sub-stage, sub-stages per term
   static constexpr bool VST = N <= 512;
   static constexpr int VUN = VST ? 1 : JT_VUNROLL;  // unroll of the batch-start W V loops
   static constexpr int KPT = VST ? VST_KPT : 0;
   static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
   static constexpr int SV_BYTES = STAGED ? V_BYTES : 0;  // v_l bytes in a ring stage (URING stages hold u~_l only)
   static constexpr int STAGE_BYTES =
-      STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : (URING_WANT ? (U_BYTES + 127) / 128 * 128 : 0);
+      SUB ? SUBB
+          : (STAGED ? (V_BYTES + U_BYTES + PH_BYTES + 127) / 128 * 128 : (URING_WANT ? (U_BYTES + 127) / 128 * 128 : 0));
   // twiddle tables of the passes after the first, copied to SMEM (TWS): every twiddle is one broadcast
   // LDS.128 instead of a chain of complex multiplies
   static constexpr bool TWS = N <= 1024;
@@ -235,10 +245,13 @@ struct Cfg {
                ? gpc_fit(g - 1, nstage)
                : g;
   }
-  static constexpr int GPC = gpc_fit(8, STAGED ? 2 : 1);  // groups per CTA (one CTA per SM)
+  static constexpr int GPC = gpc_fit(8, STAGED ? 2 : (SUB ? 4 : 1));  // groups per CTA (one CTA per SM)
   static constexpr bool URING = URING_WANT && GPC * GROUP_BYTES + hdr_bytes(1) <= SMEM_LIMIT;
-  // a third ring stage when it fits next to the GPC groups
-  static constexpr int NSTAGE = (STAGED && GPC * GROUP_BYTES + hdr_bytes(3) <= SMEM_LIMIT) ? 3 : (URING ? 1 : 2);
+  static constexpr int sub_fit(int s) { return (s > 4 && GPC * GROUP_BYTES + hdr_bytes(s) > SMEM_LIMIT) ? sub_fit(s - 1) : s; }
+  // a third ring stage when it fits next to the GPC groups; SUB: as many sub-stages as fit (<= one term)
+  static constexpr int NSTAGE = SUB ? sub_fit(12)
+                                    : ((STAGED && GPC * GROUP_BYTES + hdr_bytes(3) <= SMEM_LIMIT) ? 3 : (URING ? 1 : 2));
+  static_assert(!SUB || GPC * GROUP_BYTES + hdr_bytes(NSTAGE) <= SMEM_LIMIT, "SUB ring");
   static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES + 3 * NSTAGE * 8;  // stages + full/empty barriers + counters
   static constexpr int BINFO_OFF = (RING_BYTES + 127) / 128 * 128;
   static constexpr int TW_OFF = BINFO_OFF + BINFO_BYTES;
@@ -337,6 +350,10 @@ struct Ring {
     return reinterpret_cast<const double *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES + C::SV_BYTES + C::U_BYTES);
   }
   __device__ __forceinline__ void issue(long long seq) const {  // producer: one thread
+    if constexpr (C::SUB) {
+      issue_sub(seq);
+      return;
+    }
     const int s = (int)(seq % C::NSTAGE);
     const int l = l0 + (int)(seq % rs);
     const bool kc = C::VST && l * C::KPT < k0;  // chunk l of W V exists (zero-padded to KPT degrees)
@@ -351,9 +368,69 @@ struct Ring {
     if (kc)
       tma_load_1d(const_cast<double *>(ph(seq)), gph + (long long)l * C::KPT * C::MAXR * C::NBINS, ph_bytes, &full[s]);
   }
+  // SUB: sub-stage seq = 8 t + part of the CTA's t-th term (term l0 + t % rs); 16 KB, laid out for the consumer:
+  //   forward  part j < 4: v_l[1024 j .. 1024 j + 1023]                         (A1 of positions r in [8j, 8j + 8))
+  //            part 4 + i: [c][h][256] = u~_l rows c of bins h 1024 + 256 i + [0, 256) (A3 of bins q in [4i, 4i + 4))
+  //   inverse  part i < 4: [c][512]    = u~_l rows c of bins 512 i + [0, 512)          (bin sums of q in [4i, 4i + 4))
+  //            part 4 + j: [h][256]    = v_l[1024 h + 256 j + [0, 256)]              (outputs e with e / 4 in {2j, 2j + 1})
+  __device__ __forceinline__ void issue_sub(long long seq) const {
+    const int s = (int)(seq % C::NSTAGE);
+    const long long t = seq / C::NSUB;
+    const int part = (int)(seq % C::NSUB);
+    const int l = l0 + (int)(t % rs);
+    if (!JT_CHK(l >= 0 && l < r)) {  // (checks build: complete the phase without copying, so nobody hangs)
+      mbar_arrive_expect_tx(&full[s], 0);
+      return;
+    }
+    mbar_arrive_expect_tx(&full[s], C::SUBB);
+    char *dst = base + (long long)s * C::STAGE_BYTES;
+    const double2 *vl = gv + (long long)l * C::N;
+    const double2 *ul = gu + (long long)l * C::MAXR * C::NBINS;
+    const int j = part & 3;
+    if (C::INV ? part >= 4 : part < 4) {  // v_l
+      if constexpr (!C::INV) {
+        tma_load_1d(dst, vl + 1024 * j, 16384, &full[s]);
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) tma_load_1d(dst + 4096 * h, vl + 1024 * h + 256 * j, 4096, &full[s]);
+      }
+    } else {  // u~_l
+      if constexpr (!C::INV) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            tma_load_1d(dst + 4096 * (2 * c + h), ul + (long long)c * C::NBINS + 1024 * h + 256 * j, 4096, &full[s]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) tma_load_1d(dst + 8192 * c, ul + (long long)c * C::NBINS + 512 * j, 8192, &full[s]);
+      }
+    }
+  }
   __device__ __forceinline__ void wait_full(long long seq) const {
     mbar_wait(&full[seq % C::NSTAGE], (uint32_t)((seq / C::NSTAGE) & 1));
     __syncwarp();  // lanes may leave the try_wait loop in different iterations: reconverge
+  }
+  // SUB: every warp releases each sub-stage once its lanes' values are in registers; the last of the CTA's warps
+  // refills the slot with sub-stage seq + NSTAGE (same acq_rel counter / proxy fence protocol as release()).
+  __device__ __forceinline__ void release_warp(long long seq) const {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      const int s = (int)(seq % C::NSTAGE);
+      unsigned old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&cnt[s])) : "memory");
+      if (old == C::NWARP - 1) {
+        cnt[s] = 0;
+        if (seq + C::NSTAGE < total) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(seq + C::NSTAGE);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ const double2 *slot(long long seq) const {
+    return reinterpret_cast<const double2 *>(base + (seq % C::NSTAGE) * C::STAGE_BYTES);
   }
   // Called by every thread of every group after its end-of-term group_sync.  The group's thread 0 counts the
   // release; the LAST group to release the stage refills it (no thread ever blocks on the slowest group).
@@ -659,7 +736,7 @@ struct Ctx {
     }
     ring.l0 = l0;
     ring.rs = l1 - l0 > 0 ? l1 - l0 : 1;
-    ring.total = mine * (l1 - l0);
+    ring.total = mine * (l1 - l0) * (C::SUB ? C::NSUB : 1);
   }
   // CTA table: TPL x NB packed row ranges (j0 << 4) | count of the bins binof(vt, q) (staged configs;
   // the others read bstart from global: their register budget has no room for the extra live state)
@@ -686,7 +763,7 @@ struct Ctx {
       double2 *t = reinterpret_cast<double2 *>(smem_raw + C::TW_OFF);
       for (int i = threadIdx.x; i < TwTotal<C::N, C::R>::value; i += C::NT) t[i] = __ldg(&tw[i]);
     }
-    if constexpr (C::STAGED || C::URING) {
+    if constexpr (C::STAGED || C::URING || C::SUB) {
       if (threadIdx.x == 0) {
         for (int s = 0; s < C::NSTAGE; ++s) {
           mbar_init(&ring.full[s], 1);
@@ -795,7 +872,7 @@ struct State {
   // TMEM state only: chunk c's loads issued, the caller waits (tmem_wait_ld) before reading o
   __device__ __forceinline__ void chunk_issue(int c, double (&o)[CH]) const {
     static_assert(C::TPRIV, "chunk_issue reads the TMEM state");
-    JT_CHK((int)(taddr & 0xffff) + 32 * c + 32 <= C::TALLOC);
+    (void)JT_CHK((int)(taddr & 0xffff) + 32 * c + 32 <= C::TALLOC);
     tmem_ld_d8(taddr + 32 * c, &o[0]);
     tmem_ld_d8(taddr + 32 * c + 16, &o[8]);
   }
@@ -804,7 +881,7 @@ struct State {
 #pragma unroll
       for (int i = 0; i < CH; ++i) o[i] = (c * CH + i < S) ? reg[c * CH + i] : 0.0;
     } else if constexpr (C::TPRIV) {
-      JT_CHK((int)(taddr & 0xffff) + 32 * c + 32 <= C::TALLOC);
+      (void)JT_CHK((int)(taddr & 0xffff) + 32 * c + 32 <= C::TALLOC);
       tmem_ld_d8(taddr + 32 * c, &o[0]);
       tmem_ld_d8(taddr + 32 * c + 16, &o[8]);
       tmem_wait_ld();
@@ -914,7 +991,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
         const int k = vt + r * TPL;
         if (r * TPL < K0MAX && k < K0MAX) cx.alow[k * LG + line] = k < k0 ? av[r] : 0.0;  // zero pad: W V pairs
         // (checks: the bins every thread reads are real FFT bins)
-        if (r < NB) JT_CHK(m[r] >= 0 && m[r] < NBINS);
+        if (r < NB) (void)JT_CHK(m[r] >= 0 && m[r] < NBINS);
       }
     }
     prefetch_next_line<C, SPLIT>(in, lay, ((bt + cx.btstep) * C::GPC + cx.grp) * LG + line, nlines, vt, n);
@@ -959,7 +1036,28 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
         }
       }
       double xr[R], xi[R];
-      if constexpr (!C::STAGED && C::TPRIV && (JT_LOADS_FIRST & 1)) {
+      if constexpr (C::SUB) {
+        // A1 from the ring: sub-stage j holds v_l[1024 j ..], i.e. positions vt + r TPL for r in [8j, 8j + 8)
+        static_assert(R == 32 && TPL == 128 && State<C, R>::CH == 16, "SUB layout");
+#pragma unroll
+        for (int ch = 0; ch < State<C, R>::NCH; ++ch) {
+          double ac[State<C, R>::CH];
+          a.chunk(ch, ac);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const long long sq = seq * C::NSUB + 2 * ch + hh;
+            cx.ring.wait_full(sq);
+            const double2 *vs = cx.ring.slot(sq);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const double2 vv = vs[vt + i * TPL];
+              xr[16 * ch + 8 * hh + i] = vv.x * ac[8 * hh + i];
+              xi[16 * ch + 8 * hh + i] = vv.y * ac[8 * hh + i];
+            }
+            cx.ring.release_warp(sq);
+          }
+        }
+      } else if constexpr (!C::STAGED && C::TPRIV && (JT_LOADS_FIRST & 1)) {
         // A1, v_l from L1/L2: a chunk's loads issued between its TMEM state load and the wait for it
 #pragma unroll
         for (int ch = 0; ch < State<C, R>::NCH; ++ch) {
@@ -1002,6 +1100,35 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       }
       fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // A2
       cx.acquire_u(seq);
+      if constexpr (C::SUB) {
+        // A3 from the ring: sub-stage 4 + i holds rows c of bins h 1024 + 256 i + [0, 256), i.e. the thread's bins
+        // q in [4i, 4i + 4) (m = vt + (q / 2) TPL + (q % 2) N / 2); the Nyquist bin (q = R / 2) from L2
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const long long sq = seq * C::NSUB + 4 + i;
+          cx.ring.wait_full(sq);
+          const double2 *us = cx.ring.slot(sq);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int q = 4 * i + qq;
+            const int e = fwd_reg_of_bin<C>(q);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const double2 uu = us[(2 * c + (q & 1)) * 256 + vt + ((q >> 1) - 2 * i) * TPL];
+              y[q][c] = fma(uu.x, xr[e], y[q][c]);
+              y[q][c] = fma(-uu.y, xi[e], y[q][c]);
+            }
+          }
+          cx.ring.release_warp(sq);
+        }
+        const int e = fwd_reg_of_bin<C>(R / 2);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double2 uu = __ldg(&ax.ub[((long long)l * MAXR + c) * NBINS + C::N / 2]);
+          y[R / 2][c] = fma(uu.x, xr[e], y[R / 2][c]);
+          y[R / 2][c] = fma(-uu.y, xi[e], y[R / 2][c]);
+        }
+      } else
 #pragma unroll
       for (int q = 0; q < NB; ++q) {  // A3
         const int e = fwd_reg_of_bin<C>(q);
@@ -1142,7 +1269,42 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       // bin sums over the rows of the input bins q <= R/2 (positions > N/2 hold no rows), state read in chunks
       using YS = State<C, NB * MAXR>;
-      if constexpr (!C::STAGED && !C::VST && MAXR == 2 && (JT_LOADS_FIRST & 2) && C::N >= JT_LF_INV_NMIN) {
+      if constexpr (C::SUB) {
+        // bin sums from the ring: sub-stage i holds rows c of bins 512 i + [0, 512), i.e. the thread's input bins
+        // q in [4i, 4i + 4) (m = vt + q TPL); state chunk ch holds the rows of bins 8 ch .. 8 ch + 7
+        static_assert(R == 32 && TPL == 128 && YS::CH == 16 && YS::NCH == 3, "SUB layout");
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          double yc[YS::CH];
+          yb.chunk(ch, yc);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const long long sq = seq * C::NSUB + 2 * ch + hh;
+            cx.ring.wait_full(sq);
+            const double2 *us = cx.ring.slot(sq);
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const int q = 8 * ch + 4 * hh + qq;
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const double2 uu = us[c * 512 + vt + qq * TPL];
+                const double yv = yc[(4 * hh + qq) * 2 + c];
+                xr[q] = fma(uu.x, yv, xr[q]);
+                xi[q] = fma(uu.y, yv, xi[q]);
+              }
+            }
+            cx.ring.release_warp(sq);
+          }
+        }
+        double yc[YS::CH];
+        yb.chunk(2, yc);  // the Nyquist bin's rows (nonzero only for vt == 0), u~_l from L2
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double2 uu = __ldg(&ax.ub[((long long)l * MAXR + c) * NBINS + C::N / 2]);
+          xr[R / 2] = fma(uu.x, yc[c], xr[R / 2]);
+          xi[R / 2] = fma(uu.y, yc[c], xi[R / 2]);
+        }
+      } else if constexpr (!C::STAGED && !C::VST && MAXR == 2 && (JT_LOADS_FIRST & 2) && C::N >= JT_LF_INV_NMIN) {
         // u~_l from L1/L2: both rows' loads of every bin in flight before the state chunks
         double2 u1[NB];
 #pragma unroll
@@ -1205,6 +1367,27 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         }
       }
       fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);
+      if constexpr (C::SUB) {
+        // a[k] += Re(v_l[k] B[k]) from the ring: sub-stage 4 + j holds v_l[1024 h + 256 j + ...], i.e. the outputs
+        // e with e / RSL in {2j, 2j + 1} (k = vt + (e / RSL) TPL + (e % RSL) N / RSL, RSL = 4)
+        static_assert(C::RSL == 4, "SUB layout");
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const long long sq = seq * C::NSUB + 4 + j;
+          cx.ring.wait_full(sq);
+          const double2 *vs = cx.ring.slot(sq);
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const int e = 4 * (2 * j + tt) + h;
+              const double2 vv = vs[h * 256 + vt + tt * TPL];
+              acc[e] = fma(vv.x, xr[e], acc[e]);
+              acc[e] = fma(-vv.y, xi[e], acc[e]);
+            }
+          cx.ring.release_warp(sq);
+        }
+      } else
 #pragma unroll
       for (int e = 0; e < R; ++e) {  // a[k] += Re(v_l[k] B[k])
         const double2 vv = vl[out_pos<C>(vt, e)];

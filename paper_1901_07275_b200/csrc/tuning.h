@@ -50,6 +50,13 @@
 #ifndef JT_URING
 #define JT_URING 1  // N > 1024 forward: one-stage TMA ring for u~_l in spare SMEM
 #endif
+#ifndef JT_SUB
+#define JT_SUB 0  // N = 4096: v_l and u~_l through a ring of 16 KB sub-stages shared by the CTA's groups (SUB;
+                  // measured slower: 5.06 vs 3.54 ms at 4096^2)
+#endif
+#ifndef JT_SUB_SPLITX
+#define JT_SUB_SPLITX 1  // ... with the split exchange (one real plane at a time) to fit a ring deeper than a term
+#endif
 #ifndef JT_URING_NMAX
 #define JT_URING_NMAX 2048  // ... up to this N (2048 forward -5 %; 4096 +8 %: the stage starves L1)
 #endif
