@@ -66,6 +66,10 @@ struct AxisDev {
 struct TermSplit {
   int S;
   double *part;
+  // cluster != 0: the grid is launched in clusters of the S CTAs of a batch (cluster rank = slice), and the
+  // partial lines are summed through distributed shared memory at the end of the kernel (cluster_reduce): no
+  // workspace, no ts_reduce launch
+  int cluster;
 };
 
 // (build-time tuning knobs JT_*: tuning.h)
@@ -258,6 +262,8 @@ struct Cfg {
   static constexpr int HDR_BYTES = hdr_bytes(NSTAGE);
   static constexpr int NT = GPC * GT;  // threads per CTA
   static constexpr size_t smem_bytes() { return (size_t)HDR_BYTES + (size_t)GPC * GROUP_BYTES; }
+  // term-split partial lines of a batch (GPC LG lines x N doubles) fit in the group areas (cluster reduction)
+  static constexpr bool CLUSTER_FIT = (long long)GPC * LG * N * 8 <= (long long)GPC * GROUP_BYTES;
   __device__ static __forceinline__ int sidx(int pos, int line) { return (pos + pos / R) * LG + line; }
   static_assert(GT % 32 == 0, "group must be whole warps");
   static_assert(RSL >= 2, "last pass radix");
@@ -949,6 +955,46 @@ __device__ __forceinline__ void prefetch_next_line(const double *in, const Layou
   }
 }
 
+// Term split in clusters (TermSplit::cluster): this CTA's partial lines [line in batch][j] in its group areas.
+template <class C>
+__device__ __forceinline__ double *cluster_part() {
+  extern __shared__ __align__(128) char smem_raw[];
+  return reinterpret_cast<double *>(smem_raw + C::HDR_BYTES);
+}
+
+// Sum of the S CTAs' partial lines of this cluster's batch through distributed shared memory, in slice order (the
+// order of ts_reduce: bit-identical results), written in the plain (outer, n, inner) layout.  CTA rank s of the
+// cluster sums elements [s E / S, (s + 1) E / S) of the batch's E = lines x n.  The first cluster barrier publishes
+// every CTA's partials; the second keeps each CTA's shared memory alive until its peers have read it.
+template <class C>
+__device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts, const Layout &lay, long long nlines,
+                                               int n) {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const long long bt = blockIdx.x / ts.S;
+  const long long L0 = bt * C::GPC * C::LG;
+  const long long lines = min((long long)C::GPC * C::LG, nlines - L0);
+  const long long E = lines * n;
+  const uint32_t base = smem_u32(cluster_part<C>());
+  const long long e1 = (rank + 1) * E / ts.S;
+  for (long long e = rank * E / ts.S + threadIdx.x; e < e1; e += C::NT) {
+    double sum = 0.0;
+    for (int t = 0; t < ts.S; ++t) {
+      uint32_t ra;
+      double v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base + (uint32_t)(e * 8)), "r"(t));
+      asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+      sum += v;
+    }
+    const long long lb = e / n, j = e - lb * n, L = L0 + lb;
+    const long long o = L / lay.inner, i = L - o * lay.inner;
+    const long long idx = (o * n + j) * lay.inner + i;
+    if (JT_CHK(idx >= 0 && idx < lay.out_lim)) out[idx] = sum;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------------------------
 // Forward axis pass (K4).
 // ------------------------------------------------------------------------------------------------
@@ -1143,6 +1189,14 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       cx.release(seq);
     }
 
+    // (cluster term split: the partial lines go to this CTA's group areas once every group is done with them)
+    double *cpart = nullptr;
+    if constexpr (TSPLIT && C::CLUSTER_FIT) {
+      if (ts.cluster) {
+        __syncthreads();  // (one batch per CTA in a term-split launch: every thread is here)
+        cpart = cluster_part<C>() + (long long)(cx.grp * LG + line) * n;
+      }
+    }
     if (live) {
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
@@ -1152,7 +1206,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
           for (int c = 0; c < MAXR; ++c)
             if (c < cnt && JT_CHK(j0 + c >= 0 && j0 + c < n && L < nlines)) {
-              if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + j0 + c] = y[q][c];
+              if (TSPLIT && cpart) cpart[j0 + c] = y[q][c];
+              else if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + j0 + c] = y[q][c];
               else if (JT_CHK(oa.at(j0 + c) >= 0 && oa.at(j0 + c) < lay.out_lim)) out[oa.at(j0 + c)] = y[q][c];
             }
         }
@@ -1161,6 +1216,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
     group_sync<C>();  // alow / PRIV reuse by the next batch
   }
   cx.finish();
+  if constexpr (TSPLIT && C::CLUSTER_FIT)
+    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1408,14 +1465,26 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       group_sync<C>();
     }
 
+#pragma unroll
+    for (int e = 0; e < R; ++e) {  // the dense block's degrees
+      const int k = out_pos<C>(vt, e);
+      if (k < k0) acc[e] += cx.alow[k * LG + line];
+    }
+    double *cpart = nullptr;
+    if constexpr (TSPLIT && C::CLUSTER_FIT) {
+      if (ts.cluster) {
+        __syncthreads();  // (one batch per CTA in a term-split launch: every thread is here)
+        cpart = cluster_part<C>() + (long long)(cx.grp * LG + line) * n;
+      }
+    }
     if (live) {
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         const int k = out_pos<C>(vt, e);
-        double val = acc[e];
-        if (k < k0) val += cx.alow[k * LG + line];
+        const double val = acc[e];
         if (k < n) {
-          if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + k] = val;
+          if (TSPLIT && cpart) cpart[k] = val;
+          else if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + k] = val;
           else if (JT_CHK(oa.at(k) >= 0 && oa.at(k) < lay.out_lim)) out[oa.at(k)] = val;
         }
       }
@@ -1423,6 +1492,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
     group_sync<C>();
   }
   cx.finish();
+  if constexpr (TSPLIT && C::CLUSTER_FIT)
+    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n);
 }
 
 }  // namespace jtk

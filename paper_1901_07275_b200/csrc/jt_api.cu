@@ -60,6 +60,90 @@ struct DeviceGuard {
   }
 };
 
+// SM count of the current device (cached: a driver query per launch costs microseconds on the latency-bound
+// few-line transforms).
+int sm_count() {
+  static int cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) return 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
+// cudaFuncSetAttribute once per (kernel, attribute, device) instead of on every launch.
+struct AttrKey {
+  const void *kern;
+  int attr, dev;
+};
+std::mutex g_attr_mu;
+std::vector<AttrKey> g_attr_done;
+cudaError_t ensure_attr(const void *kern, cudaFuncAttribute attr, int value) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (auto &k : g_attr_done)
+    if (k.kern == kern && k.attr == (int)attr && k.dev == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, attr, value);
+  if (e == cudaSuccess) g_attr_done.push_back(AttrKey{kern, (int)attr, dev});
+  return e;
+}
+cudaError_t ensure_smem_attr(const void *kern, int smem) {
+  return ensure_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+// Largest cluster size S <= want (down to 2) with which kernel `kern` (smem bytes per CTA) runs `need` clusters at
+// once on this device (one wave: a second wave would double the latency-bound launch); 0 if none (then the caller
+// uses the workspace + ts_reduce path).  Cached per kernel, device and request.
+struct ClusterKey {
+  const void *kern;
+  int dev, want, need, got;
+};
+std::vector<ClusterKey> g_cluster_fit;
+int cluster_fit(const void *kern, int NT, size_t smem, int want, int need) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto &k : g_cluster_fit)
+      if (k.kern == kern && k.dev == dev && k.want == want && k.need == need) return k.got;
+  }
+  int got = 0;
+  if (ensure_smem_attr(kern, (int)smem) == cudaSuccess &&
+      (want <= 8 || ensure_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
+    for (int S = want; S >= 2 && !got; --S) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)S);
+      cfg.blockDim = dim3((unsigned)NT);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)S;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc >= need) got = S;
+    }
+  }
+  cudaGetLastError();  // (a refused query is not an error of the caller's)
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  g_cluster_fit.push_back(ClusterKey{kern, dev, want, need, got});
+  return got;
+}
+
+// Is stream s being captured into a CUDA graph?  (Then the calls skip their cross-call ordering events and
+// timing marks, and must not grow workspaces: capture after one uncaptured call of the same shape.)
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
+
 }  // namespace
 
 // ---- NCCL, loaded on first use (dlopen of libnccl.so.2: the one torch already loaded, else the system's) ----
@@ -225,6 +309,13 @@ constexpr int radix_for() {
   return radix_of(N, MAXR);
 }
 
+// The term-split instantiation of configuration C's kernel.
+template <class C>
+auto ts_kernel() {
+  if constexpr (C::INV) return jtk::inv_axis_kernel<C, false, true>;
+  else return jtk::fwd_axis_kernel<C, false, true>;
+}
+
 // Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
 template <class C>
 jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
@@ -233,18 +324,42 @@ jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
   const long long lines_per_batch = (long long)C::GPC * C::LG;
   const long long batches = (nlines + lines_per_batch - 1) / lines_per_batch;
   if (batches == 0) return JT_OK;
-  int dev = 0, sms = 148;
-  JT_CUDA_TRY(cudaGetDevice(&dev));
-  JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int sms = sm_count();
   const bool split = lay.in_cs != ax.n || lay.out_cs != ax.n;
   // few lines (fewer batches than half the SMs): split the rank terms over S CTAs per batch and sum the
   // partials (jtk::TermSplit, jtk::ts_reduce), so a latency-bound launch uses more of the GPU
-  jtk::TermSplit ts{1, nullptr};
+  jtk::TermSplit ts{1, nullptr, 0};
   if (allow_ts && !split && nlines == lay.outer * lay.inner && ax.r >= 2 && batches * 2 <= sms) {
     const int S = (int)std::min<long long>(ax.r, sms / batches);
+    if constexpr (C::CLUSTER_FIT && JT_TS_CLUSTER) {
+      // the batch's S CTAs as one thread-block cluster, partials summed through distributed shared memory inside
+      // the kernel (jtk::cluster_reduce): one launch, no workspace round trip through L2 / HBM
+      auto kern = ts_kernel<C>();
+      const int Sc = S > 1 ? cluster_fit((const void *)kern, C::NT, smem, std::min(S, JT_TS_CLUSTER_MAX), (int)batches)
+                           : 0;
+      if (Sc > 1) {
+        ts = jtk::TermSplit{Sc, nullptr, 1};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(batches * Sc));
+        cfg.blockDim = dim3((unsigned)C::NT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)Sc;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        JT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ax, in, out, nlines, lay, ts));
+        ++p->launches;
+        return JT_OK;
+      }
+    }
     const size_t need = (size_t)S * nlines * ax.n;
     if (S > 1) {
       if (p->ts_elems < need) {
+        if (capturing(s)) return fail(JT_ERR_ARG, "term-split workspace must grow: run the call once before capturing it");
         // stream-ordered: no implicit device synchronisation in the middle of a pipelined call (a ragged later
         // chunk may need more than an earlier one), and valid under CUDA graph capture
         if (p->ts_work) cudaFreeAsync(p->ts_work, s);
@@ -254,30 +369,28 @@ jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
           return fail(JT_ERR_ALLOC, "term-split workspace");
         p->ts_elems = need;
       }
-      ts = jtk::TermSplit{S, p->ts_work};
+      ts = jtk::TermSplit{S, p->ts_work, 0};
     }
   }
   const unsigned grid = ts.S > 1 ? (unsigned)(batches * ts.S) : (unsigned)std::min<long long>(batches, sms);
   if constexpr (C::WG) {  // (only reached for term-split launches: see launch_nmd)
     if (ts.S <= 1) return fail(JT_ERR_ARG, "internal: one-warp-group configuration without term split");
     if constexpr (C::INV) {
-      JT_CUDA_TRY(cudaFuncSetAttribute(jtk::inv_axis_kernel<C, false, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      JT_CUDA_TRY(ensure_smem_attr((const void *)jtk::inv_axis_kernel<C, false, true>, (int)smem));
       jtk::inv_axis_kernel<C, false, true><<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
     } else {
-      JT_CUDA_TRY(cudaFuncSetAttribute(jtk::fwd_axis_kernel<C, false, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      JT_CUDA_TRY(ensure_smem_attr((const void *)jtk::fwd_axis_kernel<C, false, true>, (int)smem));
       jtk::fwd_axis_kernel<C, false, true><<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
     }
   } else if constexpr (C::INV) {
     auto kern = ts.S > 1 ? jtk::inv_axis_kernel<C, false, true>
                          : (split ? jtk::inv_axis_kernel<C, true> : jtk::inv_axis_kernel<C, false>);
-    JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    JT_CUDA_TRY(ensure_smem_attr((const void *)kern, (int)smem));
     kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
   } else {
     auto kern = ts.S > 1 ? jtk::fwd_axis_kernel<C, false, true>
                          : (split ? jtk::fwd_axis_kernel<C, true> : jtk::fwd_axis_kernel<C, false>);
-    JT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    JT_CUDA_TRY(ensure_smem_attr((const void *)kern, (int)smem));
     kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
   }
   JT_CUDA_TRY(cudaGetLastError());
@@ -308,9 +421,7 @@ jt_status launch_nmd(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
   using C = jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, INV>;
   using CW = jtk::Cfg<N, radix_ts_of(N, MAXR), MAXR, INV, true>;
   if constexpr (CW::LG != C::LG || CW::R != C::R) {  // term-split launches: one-warp groups / their own radix
-    int dev = 0, sms = 148;
-    JT_CUDA_TRY(cudaGetDevice(&dev));
-    JT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int sms = sm_count();
     if (term_split_applies<CW>(ax, nlines, lay, allow_ts, sms)) {
       jtk::AxisDev axt = ax;
       axt.tw = ax.tw_ts;
@@ -538,6 +649,7 @@ jt_status check_device_plan(const jt_plan_s *p) {
 
 // Ordering of calls that share the plan-owned buffers: the call's stream waits for the previous call's end.
 jt_status begin_call(const jt_plan_s *p, cudaStream_t s) {
+  if (capturing(s)) return JT_OK;  // (a graph orders its own nodes; the events are recorded by uncaptured calls)
   if (!p->ev_busy) {
     JT_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_busy, cudaEventDisableTiming));
     JT_CUDA_TRY(cudaEventRecord(p->ev_busy, s));
@@ -546,6 +658,7 @@ jt_status begin_call(const jt_plan_s *p, cudaStream_t s) {
   return JT_OK;
 }
 jt_status end_call(const jt_plan_s *p, cudaStream_t s) {
+  if (capturing(s)) return JT_OK;
   JT_CUDA_TRY(cudaEventRecord(p->ev_busy, s));
   return JT_OK;
 }
@@ -554,7 +667,7 @@ jt_status end_call(const jt_plan_s *p, cudaStream_t s) {
 // 8 / 9 exchange start / end (comm stream).
 enum { PM_START = 0, PM_END = 1, PM_AX = 2, PM_XS = 8, PM_XE = 9 };
 jt_status mark(const jt_plan_s *p, int id, cudaStream_t s) {
-  if (!p->prof_on) return JT_OK;
+  if (!p->prof_on || capturing(s)) return JT_OK;
   if (!p->pev[id]) JT_CUDA_TRY(cudaEventCreate(&p->pev[id]));
   JT_CUDA_TRY(cudaEventRecord(p->pev[id], s));
   p->prec[id] = true;

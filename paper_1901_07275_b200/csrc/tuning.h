@@ -105,6 +105,12 @@
 #ifndef JT_R4096
 #define JT_R4096 32  // register radix at N = 4096 (16: forward +9 %, inverse +12 %)
 #endif
+#ifndef JT_TS_CLUSTER
+#define JT_TS_CLUSTER 1  // term-split launches as thread-block clusters reducing through DSMEM (no ts_reduce launch)
+#endif
+#ifndef JT_TS_CLUSTER_MAX
+#define JT_TS_CLUSTER_MAX 16  // largest cluster (non-portable above 8; smaller if the device cannot place it)
+#endif
 #ifndef JT_HOST_SLOTS
 #define JT_HOST_SLOTS 2  // staging slots of the *_host entry points (3: no change in the 512^3 e2e stream)
 #endif

@@ -366,11 +366,11 @@ def test_last_launches_counts_kernels():
     jt.jt_forward_axis(p.handle, 1, x, y, 128, 128)
     assert jt.jt_last_launches(p) == 1
     p.close()
-    q = jt.Plan(1024, 0.25, -0.3, 1e-12)  # one line: term split + ts_reduce
-    x1 = torch.from_numpy(si.gaussian((1024,), seed=3)).cuda()
+    q = jt.Plan(1024, 0.25, -0.3, 1e-12)  # one line: term split, reduced in a thread-block cluster (one launch)
+    x1 = torch.from_numpy(si.gaussian((1024,), seed=3)).cuda()  # or, where no cluster fits, + ts_reduce
     y1 = torch.empty_like(x1)
     jt.jt_inverse(q.handle, x1, y1)
-    assert jt.jt_last_launches(q) == 2
+    assert jt.jt_last_launches(q) in (1, 2)
     torch.cuda.synchronize()
     q.close()
 
