@@ -250,6 +250,12 @@ struct Cfg {
                : g;
   }
   static constexpr int GPC = gpc_fit(8, STAGED ? 2 : (SUB ? 4 : 1));  // groups per CTA (one CTA per SM)
+  // LATE: no group barrier at the end of a rank term; the exchange buffer's reuse is guarded by a barrier just
+  // before the next term's first exchange store (and a ring stage, where there is one, is released per warp), so a
+  // warp can run into the next term's column scale and first DFT pass ahead of its group's other warps.  Measured
+  // (tools/ab_time.py, r02i): N = 4096 forward (no ring) 3.54 -> 3.45 ms at 4096^2; everywhere else slower (the
+  // per-warp ring releases cost more than the barrier: 512^3 +3.8 %, 4096 inverse +6 %), so only there.
+  static constexpr bool LATE = JT_LATE_SYNC && !SUB && !INV && !STAGED && !URING_WANT;
   static constexpr bool URING = URING_WANT && GPC * GROUP_BYTES + hdr_bytes(1) <= SMEM_LIMIT;
   static constexpr int sub_fit(int s) { return (s > 4 && GPC * GROUP_BYTES + hdr_bytes(s) > SMEM_LIMIT) ? sub_fit(s - 1) : s; }
   // a third ring stage when it fits next to the GPC groups; SUB: as many sub-stages as fit (<= one term)
@@ -670,6 +676,7 @@ __device__ __forceinline__ void fft(double (&xr)[C::R], double (&xi)[C::R], void
 #pragma unroll
   for (int i = 0; i < P0::B; ++i) dft<P0::RS>(&xr[i * P0::RS], &xi[i * P0::RS]);
   if constexpr (!P0::LAST) {
+    if constexpr (C::LATE) group_sync<C>();  // every thread of the group has read the previous term's exchange
     do_exchange<C, 1>(xr, xi, buf, vt, line);
     run_passes<C, P0::RS>(xr, xi, buf, vt, line, tw, ttw);
   }
@@ -841,7 +848,8 @@ struct Ctx {
     if constexpr (C::URING) ring.wait_full(seq);
   }
   __device__ __forceinline__ void release(long long seq) const {
-    if constexpr (C::STAGED || C::URING) ring.release(seq, gt);
+    if constexpr ((C::STAGED || C::URING) && C::LATE) ring.release_warp(seq);
+    else if constexpr (C::STAGED || C::URING) ring.release(seq, gt);
   }
 };
 
@@ -1185,7 +1193,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
           y[q][c] = fma(-uu.y, xi[e], y[q][c]);
         }
       }
-      group_sync<C>();  // exchange buffer and this stage are free again
+      if constexpr (!C::LATE) group_sync<C>();  // exchange buffer and this stage are free again
       cx.release(seq);
     }
 
@@ -1451,10 +1459,11 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         acc[e] = fma(vv.x, xr[e], acc[e]);
         acc[e] = fma(-vv.y, xi[e], acc[e]);
       }
-      group_sync<C>();
+      if constexpr (!C::LATE) group_sync<C>();
       cx.release(seq);
     }
     if constexpr (C::VST && C::GW > 1) {  // combine the per-warp partials of degrees < kin
+      if constexpr (C::LATE) group_sync<C>();  // (every warp's last partials written)
       for (int i = cx.gt; i < kin * LG; i += C::GT) {
         const int k = i / LG, ln = i % LG;
         double s = 0.0;
