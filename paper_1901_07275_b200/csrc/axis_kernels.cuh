@@ -190,7 +190,7 @@ struct Cfg {
   static constexpr int XB = SPLITX ? 8 : 16;  // bytes per exchange slot
   // (MAXR = 4: twice the row accumulators / bin rows per thread)
   static constexpr int REGS = R >= 32 ? 255
-                                      : (PRIV ? (MAXR > 2 ? JT_REGS16M4 : (INV ? JT_REGS16 : JT_REGS16F))
+                                      : (PRIV ? (MAXR > 3 ? JT_REGS16M4 : MAXR == 3 ? JT_REGS16M3 : (INV ? JT_REGS16 : JT_REGS16F))
                                               : (MAXR > 2 ? 200 : 168));
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
   // stores and the unit-stride loads are both free of bank conflicts

@@ -442,6 +442,7 @@ template <int N>
 jt_status launch_n(const jt_plan_s *p, bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out,
                    long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
   if (maxr <= 2) return launch_nm<N, 2>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
+  if (maxr == 3) return launch_nm<N, 3>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
   return launch_nm<N, 4>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
 }
 
@@ -545,7 +546,7 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   int maxr = 0;
   for (int64_t m = 0; m < nbins; ++m) maxr = std::max(maxr, h.bstart[m + 1] - h.bstart[m]);
   if (maxr > 4) return fail(JT_ERR_NUMERIC, "more than 4 nodes share one FFT bin");
-  const int MAXR = maxr <= 2 ? 2 : 4;
+  const int MAXR = maxr <= 2 ? 2 : maxr;  // 2 (Gauss-Jacobi nodes), 3 or 4 (clustered nonuniform points)
   p->dev[axis].maxr = MAXR;
   std::vector<double2> ub((size_t)r * nbins * MAXR, make_double2(0.0, 0.0)), v((size_t)r * N), tw(N);
   std::vector<double> phivb((size_t)std::max(k0, 1) * nbins * MAXR, 0.0);

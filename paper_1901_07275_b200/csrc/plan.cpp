@@ -3,7 +3,7 @@
 //
 //   1. Gauss-Jacobi rule in t (construction deferred by the paper to
 //      [Jacobi], PAPER.md:444 -> DESIGN.md reading R3): eigenvalues of the Jacobi matrix by implicit
-//      QL (long double), Newton polish in t on p_n(cos t), weights lambda_j = 1 / sum_{k<n} p_k(x_j)^2.
+//      symmetric QR (long double), Newton polish in t on p_n(cos t), weights lambda_j = 1 / sum_{k<n} p_k(x_j)^2.
 //   2. Non-oscillatory generator P~_k + i Q~_k = M e^{i psi} at the nodes,
 //      by the Cauchy transform h0 (tanh-sinh, long double) + the three-term recurrence
 //      (reading R8 / route A5' of SURVEY.md).
@@ -621,20 +621,28 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
   // nodes never exceed it.  Clustered nonuniform points are spread greedily to the next bins (m_j stays
   // non-decreasing in j; the factorisation absorbs the larger residual t_j - 2 pi m_j / N as extra rank),
   // displacing no point by more than 2 bins; if that fails the FFT length doubles (up to the kernels' 4096).
+  // Spreading (reading R21): each point takes the first bin >= max([t_j N / 2 pi], previous point's bin) with room
+  // (bins stay non-decreasing, rows of a bin contiguous), at most 2 bins right of its rounded bin, under a cap of 3
+  // rows per bin (the kernels' MAXR = 3 instantiation: a quarter less row work than MAXR = 4), else 4; failing both,
+  // the FFT length doubles.  Gauss-Jacobi nodes (<= 2 per bin) are never moved.
   for (;;) {
-    ax.bins.assign(n, 0);
-    ax.bstart.assign(ax.N / 2 + 2, 0);
-    bool ok = true;
-    int32_t prev = 0;
-    for (int64_t j = 0; j < n && ok; ++j) {
-      const int32_t m0 = (int32_t)nearbyintl(t[j] * (ld)ax.N / (2 * PI_L));
-      int32_t m = std::max(m0, prev);
-      while (m <= ax.N / 2 && ax.bstart[m + 1] >= 4) ++m;
-      if (m > ax.N / 2 || m - m0 > 2) ok = false;
-      else {
-        ax.bins[j] = prev = m;
-        ax.bstart[m + 1]++;
+    bool ok = false;
+    for (int cap : {3, 4}) {
+      ax.bins.assign(n, 0);
+      ax.bstart.assign(ax.N / 2 + 2, 0);
+      ok = true;
+      int32_t prev = 0;
+      for (int64_t j = 0; j < n && ok; ++j) {
+        const int32_t m0 = (int32_t)nearbyintl(t[j] * (ld)ax.N / (2 * PI_L));
+        int32_t m = std::max(m0, prev);
+        while (m <= ax.N / 2 && ax.bstart[m + 1] >= cap) ++m;
+        if (m > ax.N / 2 || m - m0 > 2) ok = false;
+        else {
+          ax.bins[j] = prev = m;
+          ax.bstart[m + 1]++;
+        }
       }
+      if (ok) break;
     }
     if (ok) break;
     if (ax.N >= 4096) {

@@ -16,6 +16,9 @@
 #ifndef JT_REGS16M4
 #define JT_REGS16M4 168  // MAXR = 4 radix-16 kernels (128 spilled: nonuniform 256^3 forward 3.85 -> 3.00 ms)
 #endif
+#ifndef JT_REGS16M3
+#define JT_REGS16M3 144  // MAXR = 3 radix-16 kernels (clustered nonuniform points after the cap-3 bin spreading)
+#endif
 #ifndef JT_TPRIV
 #define JT_TPRIV 1  // per-batch state in tensor memory (tcgen05.ld/st) instead of SMEM
 #endif

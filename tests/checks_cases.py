@@ -55,7 +55,7 @@ def single_gpu_cases():
             assert relerr(p.inverse_host(x), oracle.inverse(x, a, b)) <= TOL, shape
         p.close()
         expect_clean(f"single GPU {shape}")
-    # nonuniform points (MAXR = 4 bins) and the second kind
+    # nonuniform random points (cap-3 bins: the MAXR = 3 kernels), clustered points (MAXR = 4), the second kind
     shape, a, b = (96, 80), (0.4, 0.4), (0.4, 0.4)
     pts = [si.points(n, 100 + i) for i, n in enumerate(shape)]
     p = jt.Plan(shape, a, b, 1e-12, points=pts)
@@ -63,6 +63,12 @@ def single_gpu_cases():
     assert relerr(dev(p, x), oracle.forward_ex(x, a, b, pts, 0)) <= TOL
     assert relerr(dev(p, x, adjoint=True), oracle.adjoint_ex(x, a, b, pts, 0)) <= TOL
     p.close()
+    rng = np.random.default_rng(4)  # clustered: half the points in a narrow window
+    tc = np.sort(np.concatenate([rng.uniform(0.01, 3.13, 40), rng.uniform(1.0, 1.05, 40)]))
+    pc = jt.Plan((80,), (0.2,), (0.2,), 1e-12, points=[tc])
+    xc = si.gaussian((80,), seed=9)
+    assert relerr(dev(pc, xc), oracle.forward_ex(xc, (0.2,), (0.2,), [tc], 0)) <= TOL
+    pc.close()
     q = jt.Plan(shape, a, b, 1e-12, kind=jt.JT_KIND_Q)
     assert relerr(dev(q, x), oracle.forward_ex(x, a, b, None, 1)) <= TOL
     q.close()

@@ -187,9 +187,28 @@ def test_nonuniform_plan_argument_errors():
     assert ei.value.status == jt.JT_ERR_NUMERIC
 
 
+def test_random_points_take_the_cap3_bins():
+    """Uniformly random points (the NEXT-1 bench config's recipe): the plan's spreading finds a cap-3 assignment
+    (the kernels' MAXR = 3 instantiation) at the natural FFT length where one exists within 2 bins, bins non-decreasing, every point at most 2 bins
+    right of its rounded bin (reading R21)."""
+    import seeded_inputs as si
+    caps = []
+    for i in range(3):
+        t = si.points(256, 100 + i)
+        p = jt.Plan(256, 0.4, 0.4, 1e-12, device=-2, points=[t])
+        _, _, _, bins = p.factors()
+        N = p.info()["N"]
+        disp = bins - np.rint(t * N / (2 * np.pi))
+        assert N == 256 and np.all(np.diff(bins) >= 0)
+        caps.append(int(np.bincount(bins).max()))
+        assert np.min(disp) >= 0 and np.max(disp) <= 2
+        p.close()
+    assert caps == [3, 4, 3]  # axis 1's points have a run that fits 3 per bin only beyond 2 bins: cap 4 there
+
+
 def test_clustered_points_spread_over_bins():
     """Clustered points: at most 4 rows per FFT bin, bins non-decreasing, and no point more than 2 bins from
-    its rounded bin [t_j N / 2 pi] (the greedy spreading of DESIGN.md reading R21)."""
+    its rounded bin [t_j N / 2 pi] (the spreading of DESIGN.md reading R21)."""
     n = 512
     t = random_points(n, 3, clustered=True)
     p = jt.Plan(n, 0.2, 0.2, 1e-12, device=-2, points=[t])
