@@ -167,7 +167,7 @@ struct Cfg {
   static constexpr int TPL = N / R;                                     // threads per line
   // lines per group (2 lines at TPL = 128 was measured 6 % slower at N = 4096: one 8-warp barrier domain)
   // (WG applies to TPL = 16 only: at TPL = 32 one-line warps measured slower, 1024 x 64 inverse +7 %)
-  static constexpr int LG = TPL <= 8 ? 32 / TPL : (TPL <= 32 ? (WG && TPL == 16 ? 2 : 4) : 1);
+  static constexpr int LG = TPL <= 8 ? 32 / TPL : (TPL <= 32 ? (WG && TPL == 16 ? 2 : 4) : (N == 4096 && R == 32 ? JT_LG4096 : 1));
   static constexpr int GT = TPL * LG;                                   // threads per group
   static constexpr int GW = GT / 32;                                    // warps per group
   static constexpr int NSL = LastNS<N, R>::value;                       // the last pass starts at sub-size NSL
@@ -1152,6 +1152,13 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
           }
         }
       }
+      if constexpr (!C::STAGED && !C::URING && !C::SUB && JT_UPF) {
+        // (factors from L2: the epilogue's u~_l rows requested into L1 now, the FFT hides the latency)
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+#pragma unroll
+          for (int c = 0; c < MAXR; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(ul + c * NBINS + m[q]));
+      }
       fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // A2
       cx.acquire_u(seq);
       if constexpr (C::SUB) {
@@ -1430,6 +1437,11 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
             }
           }
         }
+      }
+      if constexpr (!C::STAGED && !C::SUB && JT_UPF) {
+        // (factors from L2: the accumulation's v_l entries requested into L1 now, the FFT hides the latency)
+#pragma unroll
+        for (int e = 0; e < R; ++e) asm volatile("prefetch.global.L1 [%0];" ::"l"(vl + out_pos<C>(vt, e)));
       }
       fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);
       if constexpr (C::SUB) {

@@ -108,6 +108,13 @@
 #ifndef JT_R4096
 #define JT_R4096 32  // register radix at N = 4096 (16: forward +9 %, inverse +12 %)
 #endif
+#ifndef JT_LG4096
+#define JT_LG4096 1  // lines per group of the N = 4096 radix-32 kernels (2: no TMEM twiddles, 4096^2 3.46 -> 3.91 ms)
+#endif
+#ifndef JT_UPF
+#define JT_UPF 0  // factors from L2 (N > 1024): the post-FFT factor entries prefetched into L1 before the FFT
+                  // (measured slower: 4096^2 forward 3.46 -> 3.87 ms, inverse 3.70 -> 4.02)
+#endif
 #ifndef JT_LATE_SYNC
 #define JT_LATE_SYNC 1  // end-of-term group barrier moved before the next term's first exchange (Cfg::LATE: only
                         // the ring-less N = 4096 forward, 4096^2 -2.4 %; slower elsewhere)
