@@ -983,7 +983,46 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
                                     (size_t)(c1 - c0) * sizeof(double), (size_t)n0, cudaMemcpyDeviceToHost,
                                     p->s_d2h));
     }
-  } else if (p->dist || d == 1) {  // distributed inverse (or capacity mode) / one line: copy in, transform, copy out
+  } else if (p->dist && inverse && !lowmem) {
+    // distributed inverse (transform_dist's inverse schedule, pipelined with the copies): the y-slab arrives in KC
+    // row chunks of axis 0, each chunk's axis-2 lines (d = 3) transformed as it lands; the axis-0 pass (its lines span
+    // every row) writes the chunk-major send blocks; the exchange runs in KA row chunks of the x-slab on the comm
+    // stream, each chunk's axis-1 pass starts as its rows arrive and its x-slab rows are copied back at once
+    const int G = p->nranks;
+    const long long n0 = p->n[0], n1 = p->n[1], r = d == 3 ? p->n[2] : 1;
+    const long long R = n0 / G, c = n1 / G, yrow = c * r, xrow = n1 * r;
+    if ((st = ensure_comm_stream(p)) != JT_OK) return st;
+    const int KC = (int)std::min<long long>(8, n0);
+    for (int k = 0; k < KC; ++k) {
+      const long long q0 = n0 * k / KC, q1 = n0 * (k + 1) / KC;
+      if (q1 == q0) continue;
+      const size_t off = (size_t)(q0 * yrow), cnt = (size_t)((q1 - q0) * yrow);
+      JT_CUDA_TRY(cudaMemcpyAsync(sin + off, in_h + off, cnt * sizeof(double), cudaMemcpyHostToDevice, p->s_h2d));
+      JT_CUDA_TRY(cudaEventRecord(ev_in[k], p->s_h2d));
+      JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[k], 0));
+      if (d == 3 && (st = launch_axis(p, 2, true, sin + off, sout + off, (q1 - q0) * c, 1, s, 1, 1, -1, true, -1,
+                                      p->total - (long long)off, p->total - (long long)off)) != JT_OK)
+        return st;
+    }
+    if ((st = launch_axis(p, 0, true, d == 3 ? sout : sin, p->a2a_send, 1, yrow, s, 1, G)) != JT_OK) return st;
+    JT_CUDA_TRY(cudaEventRecord(p->ev_comm, s));
+    JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_comm, 0));
+    const int KA = (int)std::min<long long>(4, R);
+    for (int k = 0; k < KA; ++k) {
+      const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
+      if (r1 == r0) continue;
+      if ((st = all_to_all_rows(p, p->a2a_send, p->a2a_recv, r0, r1, yrow, p->s_comm)) != JT_OK) return st;
+      JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], p->s_comm));
+      JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_chunk[k], 0));
+      if ((st = launch_axis(p, 1, true, p->a2a_recv + r0 * yrow, sout + r0 * xrow, r1 - r0, r, s, G, 1, -1, true, R,
+                            p->total - r0 * yrow, p->total - r0 * xrow)) != JT_OK)
+        return st;
+      JT_CUDA_TRY(cudaEventRecord(ev_out[k], s));
+      JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[k], 0));
+      JT_CUDA_TRY(cudaMemcpyAsync(out_h + r0 * xrow, sout + r0 * xrow, (size_t)((r1 - r0) * xrow) * sizeof(double),
+                                  cudaMemcpyDeviceToHost, p->s_d2h));
+    }
+  } else if (p->dist || d == 1) {  // capacity-mode distributed plans / one line: copy in, transform, copy out
     JT_CUDA_TRY(cudaMemcpyAsync(sin, in_h, bytes, cudaMemcpyHostToDevice, p->s_h2d));
     JT_CUDA_TRY(cudaEventRecord(ev_in[0], p->s_h2d));
     JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[0], 0));

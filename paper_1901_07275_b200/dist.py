@@ -306,6 +306,12 @@ class LibSlabPlan:
         jt_inverse_host(self.handle, y_host.numpy(), x_host.numpy(), stream)
         return x_host
 
+    def inverse_host_async(self, y_host, x_host, stream=None):
+        """Enqueue an end-to-end inverse of this rank's y-slab (C: jt_inverse_host_async); valid after wait_host()."""
+        from . import jt_inverse_host_async
+        jt_inverse_host_async(self.handle, y_host.numpy(), x_host.numpy(), stream)
+        return x_host
+
     def forward_host_async(self, x_host, y_host, stream=None):
         """Enqueue an end-to-end forward of this rank's slab (C: jt_forward_host_async; consecutive calls overlap
         through the plan's two staging slots); results are valid after wait_host()."""

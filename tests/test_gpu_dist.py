@@ -157,6 +157,22 @@ def test_library_slab_host_paths_virtual_ranks(world, shape, a, b):
         zh = [torch.empty(p.x_shape, dtype=torch.float64).pin_memory() for p in grp.plans]
         run_ranks(world, lambda g: grp.plans[g].inverse_host(yh[g][0], zh[g], stream=grp.streams[g]))
         assert relerr(np.concatenate([z.numpy() for z in zh], axis=0), x) <= TOL
+        # the pipelined distributed inverse (y-slab row chunks -> axis 2 -> axis 0 -> chunked exchange -> axis 1 per
+        # chunk -> x-slab rows copied back): two calls in flight, equal to the device path up to rounding
+        ys_dev = [torch.from_numpy(yh[g][0].numpy()).cuda() for g in range(world)]
+        torch.cuda.synchronize()
+        zs_dev = run_ranks(world, lambda g: grp.plans[g].inverse(ys_dev[g], stream=grp.streams[g]))
+        za = [[torch.empty(p.x_shape, dtype=torch.float64).pin_memory() for _ in range(2)] for p in grp.plans]
+
+        def inv_async(g):
+            p, s = grp.plans[g], grp.streams[g]
+            for k in range(2):
+                p.inverse_host_async(yh[g][k], za[g][k], stream=s)
+            p.wait_host()
+        run_ranks(world, inv_async)
+        z_dev = gather_x(zs_dev)
+        for k in range(2):
+            assert relerr(np.concatenate([za[g][k].numpy() for g in range(world)], axis=0), z_dev) <= 1e-14, k
     finally:
         grp.close()
 
