@@ -1030,6 +1030,35 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     JT_CUDA_TRY(cudaEventRecord(ev_out[0], s));
     JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[0], 0));
     JT_CUDA_TRY(cudaMemcpyAsync(out_h, sout, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
+  } else if (JT_HOST_SCHED == 1 || (JT_HOST_SCHED == 2 && d == 2)) {
+    // axis 0 first: the input arrives in KC row chunks; the axis-0 pass (every line spans all rows) runs once all are
+    // in; then axes d-1..1 run in place on row chunks, each copied back as one contiguous block
+    const long long n0 = p->n[0];
+    const long long row = p->total / n0;
+    const int KC = (int)std::min<long long>(8, n0);
+    for (int c = 0; c < KC; ++c) {
+      const long long r0 = n0 * c / KC, r1 = n0 * (c + 1) / KC;
+      const size_t off = (size_t)(r0 * row), cnt = (size_t)((r1 - r0) * row);
+      JT_CUDA_TRY(cudaMemcpyAsync(sin + off, in_h + off, cnt * sizeof(double), cudaMemcpyHostToDevice, p->s_h2d));
+    }
+    JT_CUDA_TRY(cudaEventRecord(ev_in[0], p->s_h2d));
+    JT_CUDA_TRY(cudaStreamWaitEvent(s, ev_in[0], 0));
+    if ((st = launch_axis(p, 0, inverse, sin, sout, 1, row, s)) != JT_OK) return st;
+    for (int c = 0; c < KC; ++c) {
+      const long long r0 = n0 * c / KC, r1 = n0 * (c + 1) / KC;
+      const size_t off = (size_t)(r0 * row), cnt = (size_t)((r1 - r0) * row);
+      for (int axis = d - 1; axis >= 1; --axis) {
+        long long outer = r1 - r0, inner = 1;
+        for (int i = 1; i < axis; ++i) outer *= p->n[i];
+        for (int i = axis + 1; i < d; ++i) inner *= p->n[i];
+        if ((st = launch_axis(p, axis, inverse, sout + off, sout + off, outer, inner, s, 1, 1, -1, true, -1,
+                              p->total - (long long)off, p->total - (long long)off)) != JT_OK)
+          return st;
+      }
+      JT_CUDA_TRY(cudaEventRecord(ev_out[c], s));
+      JT_CUDA_TRY(cudaStreamWaitEvent(p->s_d2h, ev_out[c], 0));
+      JT_CUDA_TRY(cudaMemcpyAsync(out_h + off, sout + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, p->s_d2h));
+    }
   } else {
     const long long n0 = p->n[0];
     const long long row = p->total / n0;  // elements per axis-0 index (the axis-0 pass's line count)

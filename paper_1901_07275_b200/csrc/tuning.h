@@ -125,6 +125,12 @@
 #ifndef JT_TS_CLUSTER_MAX
 #define JT_TS_CLUSTER_MAX 16  // largest cluster (non-portable above 8; smaller if the device cannot place it)
 #endif
+#ifndef JT_HOST_SCHED
+#define JT_HOST_SCHED 2  // single-GPU *_host pipeline: 0 = axes d-1..1 on arriving row chunks, then axis 0 in column
+                         // blocks copied back pitched; 1 = axis 0 first, then row chunks copied back contiguous;
+                         // 2 = 1 for 2D, 0 for 3D (e2e streams, tools/e2e_ab.py r02p: 4096^2 4.36 -> 4.20 ms with 1,
+                         // but 512^3 24.7 -> 26.9 and 256^3 3.13 -> 3.53 ms)
+#endif
 #ifndef JT_HOST_SLOTS
 #define JT_HOST_SLOTS 2  // staging slots of the *_host entry points (3: no change in the 512^3 e2e stream)
 #endif
