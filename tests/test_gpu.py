@@ -386,3 +386,28 @@ def test_radix_per_launch_kind(shape, a, b):
     assert relerr(gpu_forward(p, x), oracle.forward(x, a, b)) <= TOL
     assert relerr(gpu_forward(p, x, inverse=True), oracle.inverse(x, a, b)) <= TOL
     p.close()
+
+
+@pytest.mark.parametrize("shape,a,b", [((64, 48, 40), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)),   # many-line passes
+                                       ((1024,), (0.25,), (-0.3,)),                          # cluster term split
+                                       ((256, 256), (0.1, -0.25), (-0.4, 0.35))])
+def test_cuda_graph_capture(shape, a, b):
+    """jt_forward / jt_inverse are capture-safe after one uncaptured call (include/jt.h streams note): a CUDA graph
+    of the call replays to the same bits as a direct call."""
+    p = jt.Plan(shape, a, b, 1e-12)
+    x = torch.from_numpy(si.gaussian(shape, seed=41)).cuda()
+    s = torch.cuda.Stream()
+    for fn in (jt.jt_forward, jt.jt_inverse):
+        y_ref = torch.empty_like(x)
+        y = torch.empty_like(x)
+        with torch.cuda.stream(s):
+            fn(p.handle, x, y_ref, s)  # sizes any workspace outside the capture
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                fn(p.handle, x, y, s)
+            y.zero_()
+            g.replay()
+            s.synchronize()
+        assert torch.equal(y, y_ref)
+    p.close()
