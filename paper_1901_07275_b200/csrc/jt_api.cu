@@ -373,7 +373,7 @@ jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
     }
   }
   const unsigned grid = ts.S > 1 ? (unsigned)(batches * ts.S) : (unsigned)std::min<long long>(batches, sms);
-  if constexpr (C::WG) {  // (only reached for term-split launches: see launch_nmd)
+  if constexpr (C::WG && !JT_WG_LARGE) {  // (only reached for term-split launches: see launch_nmd)
     if (ts.S <= 1) return fail(JT_ERR_ARG, "internal: one-warp-group configuration without term split");
     if constexpr (C::INV) {
       JT_CUDA_TRY(ensure_smem_attr((const void *)jtk::inv_axis_kernel<C, false, true>, (int)smem));
@@ -426,6 +426,11 @@ jt_status launch_nmd(const jt_plan_s *p, const jtk::AxisDev &ax, const double *i
       jtk::AxisDev axt = ax;
       axt.tw = ax.tw_ts;
       return launch_cfg<CW>(p, axt, in, out, nlines, lay, s, true);
+    }
+    if constexpr (JT_WG_LARGE && N == JT_WG_LARGE && CW::R == C::R) {  // (A/B: one-warp groups for every launch)
+      jtk::AxisDev axt = ax;
+      axt.tw = ax.tw_ts;
+      return launch_cfg<CW>(p, axt, in, out, nlines, lay, s, allow_ts);
     }
   }
   return launch_cfg<C>(p, ax, in, out, nlines, lay, s, allow_ts);

@@ -125,6 +125,10 @@
 #ifndef JT_TS_CLUSTER_MAX
 #define JT_TS_CLUSTER_MAX 16  // largest cluster (non-portable above 8; smaller if the device cannot place it)
 #endif
+#ifndef JT_WG_LARGE
+#define JT_WG_LARGE 0  // N: the one-warp-group configuration (Cfg::WG) for every launch of FFT length N, not only
+                       // the term-split ones (0: off)
+#endif
 #ifndef JT_HOST_SCHED
 #define JT_HOST_SCHED 2  // single-GPU *_host pipeline: 0 = axes d-1..1 on arriving row chunks, then axis 0 in column
                          // blocks copied back pitched; 1 = axis 0 first, then row chunks copied back contiguous;
