@@ -359,3 +359,28 @@ def test_checks_build_parity_and_no_violations():
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "CHECKS OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.parametrize("name,world,flags", [("cfg5_3d_512", 8, 0), ("cfg3_2d_4096", 8, 0), ("cfg4_3d_256", 4, 0),
+                                              ("cfg5_3d_512", 8, 1)])
+def test_full_size_distributed_virtual_ranks(name, world, flags):
+    """The BASELINE multi-GPU configs at full size through the library's distributed schedule (the launch
+    configuration bench.py runs under torchrun, G virtual ranks; flags 1 = JT_DIST_LOWMEM): the assembled y-slabs
+    against the oracle's one-by-one sums at sampled outputs (first / last element included), and the full-array round
+    trip through the distributed inverse."""
+    c = si.CONFIGS[name]
+    shape, a, b = c["n"], c["a"], c["b"]
+    grp = Group(world, shape, a, b, flags=flags)
+    try:
+        x = si.gaussian(shape, seed=0)
+        xs = x_slabs(grp, x)
+        torch.cuda.synchronize()
+        ys = run_ranks(world, lambda g: grp.plans[g].forward(xs[g], stream=grp.streams[g]))
+        y = gather_y(ys)
+        idx = si.sample_indices(shape, 24, seed=3)
+        ref = oracle.forward_at(x, a, b, idx)
+        assert relerr(y[tuple(idx.T)], ref) <= TOL
+        zs = run_ranks(world, lambda g: grp.plans[g].inverse(ys[g], stream=grp.streams[g]))
+        assert relerr(gather_x(zs), x) <= TOL
+    finally:
+        grp.close()
