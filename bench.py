@@ -339,9 +339,11 @@ def main():
         axis_ms = [med([p["axis_ms"][i] for p in prof]) for i in range(3)][:d]
         slab_phases = {"axis_ms": [round(v, 4) for v in axis_ms], "exchange_ms": round(med([p["exchange_ms"] for p in prof]), 4),
                        "call_ms": round(med([p["total_ms"] for p in prof]), 4),
+                       "exchange_mode": jt.jt_dist_mode(plan.handle),
                        "note": "rank-local CUDA events (library jt_profile), median of extra profiled steps after the "
-                               "timed region; axis 1 runs in row chunks overlapped with the all-to-all, so its span "
-                               "and the exchange span overlap"}
+                               "timed region; fused mode: the axis-1 pass stores each block into its owner's receive "
+                               "buffer (NVLink peer stores) and exchange_ms is the closing barrier; nccl_all_to_all "
+                               "mode: axis 1 runs in row chunks overlapped with the all-to-all"}
         if dist is not None:
             t = torch.tensor([slab_phases["call_ms"], slab_phases["exchange_ms"]] + axis_ms, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -438,7 +440,7 @@ def main():
         e2e = {"value": total_points / (ms_e2e * 1e-3), "unit": "coefficients/s",
                "h2d_bytes_per_step": int(8 * total_points), "d2h_bytes_per_step": int(8 * total_points),
                "ms_per_step": ms_e2e, "api": "jt_forward_host_async x steps + jt_host_wait on the distributed plan per rank (pinned "
-                                             "slabs; H2D + passes + NCCL all-to-all + D2H), host wall clock, max over ranks"}
+                                             "slabs; H2D + passes + slab exchange + D2H), host wall clock, max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

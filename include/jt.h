@@ -188,9 +188,22 @@ jt_status jt_plan_dist(jt_plan_t *out, int d, const int64_t n[], const double a[
  *                   DESTROYED (undefined afterwards); per-GPU memory is the caller's two slabs + the plan's factors
  *                   (a few MB per axis) + NCCL's own buffers: 4096^3 on 8 GPUs needs 2 x 68.7 GB per GPU.  The
  *                   *_host variants stage through one plan-owned pair of slabs (copy in, transform, copy out). */
-enum { JT_DIST_LOWMEM = 1 };
+/*   JT_DIST_NCCL_A2A  use the NCCL all-to-all (grouped ncclSend / ncclRecv in row chunks, pipelined with the
+ *                   adjacent pass).  Default (flag clear, pipelined mode): the FUSED exchange where peer memory works --
+ *                   every rank's receive buffer is mapped into the other ranks (CUDA IPC, peer access over NVLink /
+ *                   NVSwitch; ranks of one node), and the axis pass that produces the chunk-major blocks (forward: axis
+ *                   1, inverse: axis 0) stores each block straight into the receive buffer of the rank that owns it,
+ *                   so the transfer overlaps the pass line by line and no all-to-all runs; two one-element NCCL
+ *                   all-reduces bracket it as barriers.  If any rank cannot map a peer, every rank falls back to the
+ *                   NCCL all-to-all (the setup is collective). */
+enum { JT_DIST_LOWMEM = 1, JT_DIST_NCCL_A2A = 2 };
 jt_status jt_plan_dist_ex(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[], double eps,
                           const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks, int flags);
+
+/* How the plan exchanges its slabs: JT_MODE_SINGLE (not distributed), JT_MODE_FUSED (the fused peer-store exchange),
+ * JT_MODE_A2A (the NCCL all-to-all), JT_MODE_LOWMEM (capacity mode: NCCL all-to-all between the caller's slabs). */
+enum { JT_MODE_SINGLE = 0, JT_MODE_FUSED = 1, JT_MODE_A2A = 2, JT_MODE_LOWMEM = 3 };
+jt_status jt_dist_mode(jt_plan_t p, int *mode);
 
 /* Wait until the work enqueued on `cuda_stream` has finished.  On a distributed plan the communicator is polled
  * meanwhile (ncclCommGetAsyncError): a failed or dead peer returns JT_ERR_NCCL (the communicator is aborted and

@@ -36,11 +36,12 @@ EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_k
             "jt_forward", "jt_inverse", "jt_forward_host", "jt_inverse_host",
             "jt_forward_axis", "jt_inverse_axis", "jt_axis_pass", "jt_axis_pass_ex", "jt_destroy", "jt_plan_rank", "jt_plan_info",
             "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_launches", "jt_last_error", "jt_version",
-            "jt_plan_dist_ex", "jt_sync", "jt_profile", "jt_last_profile",
+            "jt_plan_dist_ex", "jt_sync", "jt_profile", "jt_last_profile", "jt_dist_mode",
             "jt_debug_modified_pq", "jt_debug_checks", "jt_debug_vgroup_create", "jt_debug_vgroup_destroy",
             "jt_debug_plan_virtual", "jt_debug_axis_pass_lim"]
 
 JT_DIST_LOWMEM = 1
+JT_DIST_NCCL_A2A = 2  # the NCCL all-to-all instead of the fused (peer-store) exchange
 
 
 class JTError(RuntimeError):
@@ -68,6 +69,7 @@ _lib.jt_plan_dist.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ct
 _lib.jt_plan_dist_ex.argtypes = [ctypes.POINTER(_P), ctypes.c_int, _I64, _D, _D, ctypes.c_double,
                                  ctypes.POINTER(jt_opts), ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
 _lib.jt_sync.argtypes = [_P, ctypes.c_void_p]
+_lib.jt_dist_mode.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
 _lib.jt_profile.argtypes = [_P, ctypes.c_int]
 _lib.jt_last_profile.argtypes = [_P, _D]
 _lib.jt_debug_checks.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_ulonglong),
@@ -295,6 +297,16 @@ def jt_host_wait(plan: int):
         _check(_lib.jt_host_wait(plan), "jt_host_wait")
     finally:
         _INFLIGHT.pop(plan, None)
+
+
+DIST_MODES = {0: "single", 1: "fused", 2: "nccl_all_to_all", 3: "lowmem"}
+
+
+def jt_dist_mode(plan: int) -> str:
+    """'single', 'fused' (peer-store exchange), 'nccl_all_to_all' or 'lowmem' (C: jt_dist_mode)."""
+    m = ctypes.c_int()
+    _check(_lib.jt_dist_mode(plan, ctypes.byref(m)), "jt_dist_mode")
+    return DIST_MODES[m.value]
 
 
 def jt_sync(plan: int, stream=None):

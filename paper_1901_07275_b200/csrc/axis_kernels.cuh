@@ -917,29 +917,36 @@ __device__ __forceinline__ void load_rows(const double *__restrict__ p, int stri
 // layout of the slab all-to-all (cs = n / G chunk length),
 //     (j / cs) (outer cs inner) + o cs inner + (j % cs) inner + i,
 // which for cs == n is the plain layout.  The layout flag is uniform per launch.
+constexpr int MAX_SPLIT = 32;  // chunk-major blocks per axis (in_split / out_split, the ranks of a slab exchange)
 struct Layout {
   long long outer, inner;
   int in_cs, out_cs;  // chunk length of the input / output along the axis (== n: plain C-order)
   long long ostride;  // outer extent of the chunk-major blocks (== outer, or the whole slab when a launch
                       // covers only part of its rows: the pipelined all-to-all of the distributed forward)
   long long in_lim, out_lim;  // elements readable / writable from the in / out pointers (JT_CHECKS builds)
+  // element offset of chunk-major block g from the in / out pointer (g < split): g ostride cs inner for one
+  // buffer, or (out_peer) the block's place in ANOTHER allocation -- rank g's receive buffer mapped over NVLink
+  // (CUDA IPC), so the pass stores each block straight into the peer that owns it (the fused slab exchange)
+  long long itab[MAX_SPLIT], otab[MAX_SPLIT];
+  int out_peer;
 };
 
 
 // SPLIT is a template flag (a separate kernel instantiation) so that the plain layout costs no registers.
 template <bool SPLIT>
 struct LineAddr {
-  long long b0, cstride, inner;
+  long long b0, inner;
   int cs;
-  __device__ __forceinline__ LineAddr(long long L, long long outer, long long inner_, int n, int cs_) {
+  const long long *tab;  // Layout::itab / otab (kernel parameter space: the Layout is a __grid_constant__)
+  __device__ __forceinline__ LineAddr(long long L, const long long *tab_, long long inner_, int n, int cs_) {
     const long long o = L / inner_, i = L - o * inner_;
     inner = inner_;
     cs = SPLIT ? cs_ : n;
     b0 = o * (long long)cs * inner_ + i;
-    cstride = SPLIT ? outer * (long long)cs * inner_ : 0;  // outer = Layout::ostride (see the kernels)
+    tab = tab_;
   }
   __device__ __forceinline__ long long at(int j) const {
-    if constexpr (SPLIT) return b0 + (long long)(j / cs) * cstride + (long long)(j % cs) * inner;
+    if constexpr (SPLIT) return b0 + tab[j / cs] + (long long)(j % cs) * inner;
     else return b0 + (long long)j * inner;
   }
 };
@@ -954,7 +961,7 @@ __device__ __forceinline__ void prefetch_next_line(const double *in, const Layou
     if (L >= nlines) return;
     const bool mine = lay.inner == 1 ? (vt % 16 == 0) : (lay.inner % 16 == 0 ? (L % 16 == 0) : true);
     if (!mine) return;
-    const LineAddr<SPLIT> ia(L, lay.ostride, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> ia(L, lay.itab, lay.inner, n, lay.in_cs);
 #pragma unroll
     for (int r = 0; r < C::R; ++r) {
       const int k = vt + r * C::TPL;
@@ -1008,7 +1015,8 @@ __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts,
 // ------------------------------------------------------------------------------------------------
 template <class C, bool SPLIT, bool TSPLIT = false>
 __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, Layout lay, TermSplit ts) {
+                                                             long long nlines, const __grid_constant__ Layout lay,
+                                                             TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
@@ -1026,8 +1034,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
-    const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.itab, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.otab, lay.inner, n, lay.out_cs);
 
     // coefficients at the first-pass input positions k = vt + r TPL; degrees < k0 also to alow
     // (all loads issued before any shared-memory store, so that their latencies overlap)
@@ -1223,7 +1231,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
             if (c < cnt && JT_CHK(j0 + c >= 0 && j0 + c < n && L < nlines)) {
               if (TSPLIT && cpart) cpart[j0 + c] = y[q][c];
               else if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + j0 + c] = y[q][c];
-              else if (JT_CHK(oa.at(j0 + c) >= 0 && oa.at(j0 + c) < lay.out_lim)) out[oa.at(j0 + c)] = y[q][c];
+              else if (JT_CHK(lay.out_peer || (oa.at(j0 + c) >= 0 && oa.at(j0 + c) < lay.out_lim)))
+                out[oa.at(j0 + c)] = y[q][c];
             }
         }
       }
@@ -1240,7 +1249,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 // ------------------------------------------------------------------------------------------------
 template <class C, bool SPLIT, bool TSPLIT = false>
 __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, Layout lay, TermSplit ts) {
+                                                             long long nlines, const __grid_constant__ Layout lay,
+                                                             TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
@@ -1260,8 +1270,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
-    const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.itab, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.otab, lay.inner, n, lay.out_cs);
 
     State<C, NB * MAXR> yb(cx.priv, cx.gt, cx.taddr);  // element q MAXR + c: row c of input bin q
     {
@@ -1506,7 +1516,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         if (k < n) {
           if (TSPLIT && cpart) cpart[k] = val;
           else if (TSPLIT) ts.part[((long long)cx.slice * nlines + L) * n + k] = val;
-          else if (JT_CHK(oa.at(k) >= 0 && oa.at(k) < lay.out_lim)) out[oa.at(k)] = val;
+          else if (JT_CHK(lay.out_peer || (oa.at(k) >= 0 && oa.at(k) < lay.out_lim))) out[oa.at(k)] = val;
         }
       }
     }

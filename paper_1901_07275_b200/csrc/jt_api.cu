@@ -150,7 +150,7 @@ bool capturing(cudaStream_t s) {
 namespace nccl {
 typedef struct { char internal[128]; } UniqueId;
 typedef void *Comm;
-enum { Success = 0, Float64 = 8, InProgress = 7 };
+enum { Success = 0, Float64 = 8, InProgress = 7, Uint8 = 1, Int32 = 2, Sum = 0, Min = 3 };
 struct Api {
   bool ok = false;
   std::string why;
@@ -161,6 +161,8 @@ struct Api {
   int (*CommGetAsyncError)(Comm, int *) = nullptr;
   int (*Send)(const void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*Recv)(void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*AllGather)(const void *, void *, size_t, int, Comm, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void *, void *, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*GroupStart)() = nullptr;
   int (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(int) = nullptr;
@@ -180,11 +182,13 @@ Api &api() {
     r.CommGetAsyncError = (int (*)(Comm, int *))dlsym(h, "ncclCommGetAsyncError");
     r.Send = (int (*)(const void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclSend");
     r.Recv = (int (*)(void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclRecv");
+    r.AllGather = (int (*)(const void *, void *, size_t, int, Comm, cudaStream_t))dlsym(h, "ncclAllGather");
+    r.AllReduce = (int (*)(const void *, void *, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclAllReduce");
     r.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
     r.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
     r.GetErrorString = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
     r.ok = r.GetUniqueId && r.CommInitRank && r.CommDestroy && r.CommAbort && r.CommGetAsyncError && r.Send &&
-           r.Recv && r.GroupStart && r.GroupEnd && r.GetErrorString;
+           r.Recv && r.AllGather && r.AllReduce && r.GroupStart && r.GroupEnd && r.GetErrorString;
     if (!r.ok) r.why = "libnccl.so.2 lacks a required symbol";
     return r;
   }();
@@ -220,7 +224,14 @@ struct jt_plan_s {
   nccl::Comm comm = nullptr;
   jt_vgroup_s *vgroup = nullptr;  // test-only in-process exchange (include/jt_debug.h) instead of NCCL
   bool broken = false;     // a failed exchange aborted the communicator: every later call is JT_ERR_NCCL
-  double *a2a_send = nullptr, *a2a_recv = nullptr;  // (not allocated with JT_DIST_LOWMEM)
+  double *a2a_send = nullptr, *a2a_recv = nullptr;  // (not allocated with JT_DIST_LOWMEM; no send buffer with p2p)
+  // fused slab exchange (the default where peer memory works): every rank's receive buffer mapped into every other
+  // rank (CUDA IPC over NVLink; the virtual group: same-process pointers); the pass before the exchange stores each
+  // chunk-major block straight into its owner's receive buffer, bracketed by two tiny barriers (dist_barrier)
+  bool p2p = false;
+  double *peer_recv[jtk::MAX_SPLIT] = {};
+  bool peer_ipc[jtk::MAX_SPLIT] = {};  // peer_recv[g] was opened with cudaIpcOpenMemHandle (closed at destroy)
+  double *bar_buf = nullptr;           // one double for the NCCL barrier (an all-reduce)
   mutable cudaStream_t s_comm = nullptr;  // the pipelined all-to-all's stream (created on first use)
   mutable cudaEvent_t ev_chunk[8] = {}, ev_comm = nullptr;
   // plan-owned buffers (staging, all-to-all, term-split workspace) are reused by every call: a call's first
@@ -454,11 +465,13 @@ jt_status launch_n(const jt_plan_s *p, bool inverse, int maxr, const jtk::AxisDe
 // One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
 // layout of the slab all-to-all for the input / output.
 // in_lim / out_lim: elements of the input / output buffers from the given pointers (bounds of the JT_CHECKS
-// build; -1: the extent the geometry addresses).
+// build; -1: the extent the geometry addresses).  peer_off: out_split element offsets of the output blocks from
+// `out` when they live in other allocations (the fused slab exchange: each block stored into its rank's receive
+// buffer over NVLink); nullptr: one buffer, block g at g ostride (n / out_split) inner.
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
                       long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
                       long long nlines_only = -1, bool allow_ts = true, long long ostride = -1,
-                      long long in_lim = -1, long long out_lim = -1) {
+                      long long in_lim = -1, long long out_lim = -1, const long long *peer_off = nullptr) {
   jtk::AxisDev ax = axis_dev(p, axis);
   const int maxr = p->dev[axis].maxr;
   // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
@@ -466,8 +479,24 @@ jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *
   const long long ost = ostride >= 0 ? ostride : outer;
   const long long n = p->n[axis];
   const long long geo_in = (in_split > 1 ? ost : outer) * n * inner, geo_out = (out_split > 1 ? ost : outer) * n * inner;
-  const jtk::Layout lay{outer, inner, (int)(n / in_split), (int)(n / out_split), ost,
-                        in_lim >= 0 ? in_lim : geo_in, out_lim >= 0 ? out_lim : geo_out};
+  if (in_split > jtk::MAX_SPLIT || out_split > jtk::MAX_SPLIT) return fail(JT_ERR_ARG, "in_split / out_split > 32");
+  if (peer_off && out_split == 1) {  // one block (a world of one): the plain layout at that block's place
+    out += peer_off[0];
+    peer_off = nullptr;
+  }
+  jtk::Layout lay;
+  lay.outer = outer;
+  lay.inner = inner;
+  lay.in_cs = (int)(n / in_split);
+  lay.out_cs = (int)(n / out_split);
+  lay.ostride = ost;
+  lay.in_lim = in_lim >= 0 ? in_lim : geo_in;
+  lay.out_lim = out_lim >= 0 ? out_lim : geo_out;
+  for (int g = 0; g < jtk::MAX_SPLIT; ++g) {
+    lay.itab[g] = g < in_split ? g * ost * lay.in_cs * inner : 0;
+    lay.otab[g] = g < out_split ? (peer_off ? peer_off[g] : g * ost * lay.out_cs * inner) : 0;
+  }
+  lay.out_peer = peer_off != nullptr;
   switch (ax.N) {
     case 16: return launch_n<16>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
     case 32: return launch_n<32>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
@@ -517,6 +546,10 @@ void free_device(jt_plan_s *p) {
   cudaFree(p->ts_work);
   p->ts_work = nullptr;
   p->ts_elems = 0;
+  for (int g = 0; g < jtk::MAX_SPLIT; ++g)
+    if (p->peer_ipc[g]) cudaIpcCloseMemHandle(p->peer_recv[g]), p->peer_ipc[g] = false;
+  cudaFree(p->bar_buf);
+  p->bar_buf = nullptr;
   cudaFree(p->a2a_send);
   cudaFree(p->a2a_recv);
   p->a2a_send = p->a2a_recv = nullptr;
@@ -742,6 +775,42 @@ jt_status all_to_all_rows(const jt_plan_s *p, const double *send, double *recv, 
   return poll_comm(p);
 }
 
+// Barrier of the fused exchange on stream s: every rank's stream has reached this point before any continues
+// (NCCL: a one-double all-reduce; virtual group: cross-stream events + the host barrier).  Before the pass that
+// stores into the peers' receive buffers it guarantees the peers are done reading them (their previous call's
+// last pass); after it, that every peer's stores into this rank's receive buffer are complete.
+jt_status dist_barrier(const jt_plan_s *p, cudaStream_t s) {
+  if (p->vgroup) {
+    jt_vgroup_s *V = p->vgroup;
+    JT_CUDA_TRY(cudaEventRecord(V->ev_ready[p->rank], s));
+    if (!V->barrier()) return mark_broken(p, "virtual barrier: a peer did not arrive");
+    for (int g = 0; g < V->G; ++g) JT_CUDA_TRY(cudaStreamWaitEvent(s, V->ev_ready[g], 0));
+    if (!V->barrier()) return mark_broken(p, "virtual barrier: a peer did not arrive");
+    return JT_OK;
+  }
+  nccl::Api &A = nccl::api();
+  const int e = A.AllReduce(p->bar_buf, p->bar_buf, 1, nccl::Float64, nccl::Sum, p->comm, s);
+  if (e != nccl::Success) return mark_broken(p, std::string("barrier all-reduce: ") + A.GetErrorString(e));
+  return poll_comm(p);
+}
+
+// Offsets (elements, from this rank's receive buffer, the launch's `out`) of the blocks this rank stores into each
+// rank's receive buffer: block `rank` of rank g's buffer, rows from `rowoff`.  The virtual group resolves its
+// members' buffers here (they exist once every member's plan is built).
+jt_status peer_offsets(const jt_plan_s *p, long long rowoff, long long off[]) {
+  const long long chunk = p->total / p->nranks;
+  for (int g = 0; g < p->nranks; ++g) {
+    const double *base = p->peer_recv[g];
+    if (p->vgroup) {
+      std::lock_guard<std::mutex> lk(p->vgroup->mu);
+      base = p->vgroup->member[g] ? p->vgroup->member[g]->a2a_recv : nullptr;
+    }
+    if (!base) return fail(JT_ERR_ARG, "fused exchange: rank " + std::to_string(g) + " has no plan yet");
+    off[g] = (long long)(base - p->a2a_recv) + p->rank * chunk + rowoff;
+  }
+  return JT_OK;
+}
+
 // Slab schedule of a distributed plan (the C twin of paper_1901_07275_b200/dist.py SlabPlan):
 //   forward: axes d-1..1 on the x-slab (axis 1 written chunk-major), all-to-all, axis 0 on the y-slab; the
 //            axis-1 pass and the all-to-all are pipelined over KA row chunks of the slab: chunk k's rows are
@@ -779,6 +848,33 @@ jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, dou
     if ((st = mark(p, PM_AX + 2 * ax2, s)) != JT_OK) return st;
     if (inverse) st = launch_axis(p, 1, true, work, out, R, r, s, G, 1);
     else st = launch_axis(p, 0, false, work, out, 1, c * r, s);
+    if (st != JT_OK) return st;
+    return mark(p, PM_AX + 2 * ax2 + 1, s);
+  }
+  if (p->p2p) {
+    // fused exchange: the pass before it stores every chunk-major block straight into the receive buffer of the rank
+    // that owns it (over NVLink), so the transfer overlaps the pass line by line; two barriers bracket it
+    long long off[jtk::MAX_SPLIT];
+    if ((st = peer_offsets(p, 0, off)) != JT_OK) return st;
+    if (d == 3) {
+      if ((st = mark(p, PM_AX + 4, s)) != JT_OK) return st;
+      if ((st = launch_axis(p, 2, inverse, in, out, inverse ? n0 * c : R * n1, 1, s)) != JT_OK) return st;
+      if ((st = mark(p, PM_AX + 5, s)) != JT_OK) return st;
+    }
+    const double *src = d == 3 ? out : in;
+    if ((st = dist_barrier(p, s)) != JT_OK) return st;  // the peers are done reading their receive buffers
+    const int ax1 = inverse ? 0 : 1, ax2 = inverse ? 1 : 0;
+    if ((st = mark(p, PM_AX + 2 * ax1, s)) != JT_OK) return st;
+    if (inverse) st = launch_axis(p, 0, true, src, p->a2a_recv, 1, c * r, s, 1, G, -1, true, -1, -1, -1, off);
+    else st = launch_axis(p, 1, false, src, p->a2a_recv, R, r, s, 1, G, -1, true, -1, -1, -1, off);
+    if (st != JT_OK) return st;
+    if ((st = mark(p, PM_AX + 2 * ax1 + 1, s)) != JT_OK) return st;
+    if ((st = mark(p, PM_XS, s)) != JT_OK) return st;
+    if ((st = dist_barrier(p, s)) != JT_OK) return st;  // every rank's blocks have landed here
+    if ((st = mark(p, PM_XE, s)) != JT_OK) return st;
+    if ((st = mark(p, PM_AX + 2 * ax2, s)) != JT_OK) return st;
+    if (inverse) st = launch_axis(p, 1, true, p->a2a_recv, out, R, r, s, G, 1);
+    else st = launch_axis(p, 0, false, p->a2a_recv, out, 1, c * r, s);
     if (st != JT_OK) return st;
     return mark(p, PM_AX + 2 * ax2 + 1, s);
   }
@@ -952,6 +1048,7 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     const long long R = n0 / G, c = n1 / G, xrow = n1 * r, yrow = c * r;
     if ((st = ensure_comm_stream(p)) != JT_OK) return st;
     const int KA = (int)std::min<long long>(4, R);
+    if (p->p2p && (st = dist_barrier(p, s)) != JT_OK) return st;  // (fused exchange: peers done with their buffers)
     for (int k = 0; k < KA; ++k) {
       const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
       if (r1 == r0) continue;
@@ -966,6 +1063,14 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
           return st;
         src1 = sout + off;
       }
+      if (p->p2p) {  // this chunk's rows of every block straight into their owners' receive buffers
+        long long poff[jtk::MAX_SPLIT];
+        if ((st = peer_offsets(p, r0 * c * r, poff)) != JT_OK) return st;
+        if ((st = launch_axis(p, 1, false, src1, p->a2a_recv, r1 - r0, r, s, 1, G, -1, true, R,
+                              p->total - (long long)off, -1, poff)) != JT_OK)
+          return st;
+        continue;
+      }
       if ((st = launch_axis(p, 1, false, src1, p->a2a_send + r0 * c * r, r1 - r0, r, s, 1, G, -1, true, R,
                             p->total - (long long)off, p->total - r0 * c * r)) != JT_OK)
         return st;
@@ -973,8 +1078,12 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
       JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_chunk[k], 0));
       if ((st = all_to_all_rows(p, p->a2a_send, p->a2a_recv, r0, r1, c * r, p->s_comm)) != JT_OK) return st;
     }
-    JT_CUDA_TRY(cudaEventRecord(p->ev_comm, p->s_comm));
-    JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
+    if (p->p2p) {
+      if ((st = dist_barrier(p, s)) != JT_OK) return st;  // every rank's rows have landed here
+    } else {
+      JT_CUDA_TRY(cudaEventRecord(p->ev_comm, p->s_comm));
+      JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_comm, 0));
+    }
     const int KC = (int)std::min<long long>(8, yrow);
     for (int cb = 0; cb < KC; ++cb) {
       const long long c0 = yrow * cb / KC, c1 = yrow * (cb + 1) / KC;
@@ -997,6 +1106,7 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
     const long long n0 = p->n[0], n1 = p->n[1], r = d == 3 ? p->n[2] : 1;
     const long long R = n0 / G, c = n1 / G, yrow = c * r, xrow = n1 * r;
     if ((st = ensure_comm_stream(p)) != JT_OK) return st;
+    if (p->p2p && (st = dist_barrier(p, s)) != JT_OK) return st;  // (fused exchange: peers done with their buffers)
     const int KC = (int)std::min<long long>(8, n0);
     for (int k = 0; k < KC; ++k) {
       const long long q0 = n0 * k / KC, q1 = n0 * (k + 1) / KC;
@@ -1009,16 +1119,27 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
                                       p->total - (long long)off, p->total - (long long)off)) != JT_OK)
         return st;
     }
-    if ((st = launch_axis(p, 0, true, d == 3 ? sout : sin, p->a2a_send, 1, yrow, s, 1, G)) != JT_OK) return st;
-    JT_CUDA_TRY(cudaEventRecord(p->ev_comm, s));
-    JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_comm, 0));
+    if (p->p2p) {  // the axis-0 pass stores every block straight into its owner's receive buffer
+      long long poff[jtk::MAX_SPLIT];
+      if ((st = peer_offsets(p, 0, poff)) != JT_OK) return st;
+      if ((st = launch_axis(p, 0, true, d == 3 ? sout : sin, p->a2a_recv, 1, yrow, s, 1, G, -1, true, -1, -1, -1,
+                            poff)) != JT_OK)
+        return st;
+      if ((st = dist_barrier(p, s)) != JT_OK) return st;  // every rank's blocks have landed here
+    } else {
+      if ((st = launch_axis(p, 0, true, d == 3 ? sout : sin, p->a2a_send, 1, yrow, s, 1, G)) != JT_OK) return st;
+      JT_CUDA_TRY(cudaEventRecord(p->ev_comm, s));
+      JT_CUDA_TRY(cudaStreamWaitEvent(p->s_comm, p->ev_comm, 0));
+    }
     const int KA = (int)std::min<long long>(4, R);
     for (int k = 0; k < KA; ++k) {
       const long long r0 = R * k / KA, r1 = R * (k + 1) / KA;
       if (r1 == r0) continue;
-      if ((st = all_to_all_rows(p, p->a2a_send, p->a2a_recv, r0, r1, yrow, p->s_comm)) != JT_OK) return st;
-      JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], p->s_comm));
-      JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_chunk[k], 0));
+      if (!p->p2p) {
+        if ((st = all_to_all_rows(p, p->a2a_send, p->a2a_recv, r0, r1, yrow, p->s_comm)) != JT_OK) return st;
+        JT_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], p->s_comm));
+        JT_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_chunk[k], 0));
+      }
       if ((st = launch_axis(p, 1, true, p->a2a_recv + r0 * yrow, sout + r0 * xrow, r1 - r0, r, s, G, 1, -1, true, R,
                             p->total - r0 * yrow, p->total - r0 * xrow)) != JT_OK)
         return st;
@@ -1334,6 +1455,61 @@ jt_status jt_dist_unique_id(void *nccl_unique_id) {
   return JT_OK;
 }
 
+// Fused-exchange setup (collective over the plan's communicator): every rank's receive buffer is exported as a CUDA
+// IPC handle, the handles all-gathered, the peers' buffers opened (peer access over NVLink / NVSwitch); an all-reduce
+// (min) of the outcome makes every rank use the fused exchange, or every rank fall back to the NCCL all-to-all.
+static bool setup_ipc(jt_plan_s *p) {
+  nccl::Api &A = nccl::api();
+  const int G = p->nranks, me = p->rank;
+  const size_t H = sizeof(cudaIpcMemHandle_t);
+  int ok = 1;
+  cudaIpcMemHandle_t mine;
+  std::memset(&mine, 0, H);
+  if (cudaIpcGetMemHandle(&mine, p->a2a_recv) != cudaSuccess) ok = 0;
+  char *dbuf = nullptr;
+  int *dflag = nullptr;
+  cudaStream_t st = nullptr;
+  if (cudaMalloc((void **)&dbuf, G * H) != cudaSuccess || cudaMalloc((void **)&dflag, sizeof(int)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    ok = 0;  // (still takes part in the collectives below with whatever it has)
+  }
+  std::vector<cudaIpcMemHandle_t> all(G);
+  if (dbuf && dflag && st) {
+    cudaMemcpy(dbuf + me * H, &mine, H, cudaMemcpyHostToDevice);
+    if (A.AllGather(dbuf + me * H, dbuf, H, nccl::Uint8, p->comm, st) != nccl::Success) ok = 0;
+    cudaMemcpyAsync(all.data(), dbuf, G * H, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    for (int g = 0; g < G && ok; ++g) {
+      if (g == me) continue;
+      void *ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, all[g], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        ok = 0;
+        cudaGetLastError();
+      } else {
+        p->peer_recv[g] = static_cast<double *>(ptr);
+        p->peer_ipc[g] = true;
+      }
+    }
+    p->peer_recv[me] = p->a2a_recv;
+    cudaMemcpy(dflag, &ok, sizeof(int), cudaMemcpyHostToDevice);
+    if (A.AllReduce(dflag, dflag, 1, nccl::Int32, nccl::Min, p->comm, st) != nccl::Success) ok = 0;
+    int agreed = 0;
+    cudaMemcpyAsync(&agreed, dflag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    ok = ok && agreed;
+  }
+  if (!ok) {
+    for (int g = 0; g < G; ++g)
+      if (p->peer_ipc[g]) cudaIpcCloseMemHandle(p->peer_recv[g]), p->peer_ipc[g] = false;
+    for (auto &q : p->peer_recv) q = nullptr;
+  }
+  cudaFree(dbuf);
+  cudaFree(dflag);
+  if (st) cudaStreamDestroy(st);
+  cudaGetLastError();
+  return ok != 0;
+}
+
 // Shared by jt_plan_dist_ex (NCCL communicator) and jt_debug_plan_virtual (in-process group).
 static jt_status plan_dist_common(jt_plan_t *out, int d, const int64_t n[], const double a[], const double b[],
                                   double eps, const jt_opts *opts, int rank, int nranks, int flags,
@@ -1343,7 +1519,8 @@ static jt_status plan_dist_common(jt_plan_t *out, int d, const int64_t n[], cons
   if (d != 2 && d != 3) return fail(JT_ERR_ARG, "distributed plans need d = 2 or 3");
   if ((!nccl_unique_id && !group) || nranks < 1 || rank < 0 || rank >= nranks)
     return fail(JT_ERR_ARG, "bad rank / nranks / id");
-  if (flags & ~JT_DIST_LOWMEM) return fail(JT_ERR_ARG, "unknown JT_DIST_* flag");
+  if (flags & ~(JT_DIST_LOWMEM | JT_DIST_NCCL_A2A)) return fail(JT_ERR_ARG, "unknown JT_DIST_* flag");
+  if (nranks > jtk::MAX_SPLIT) return fail(JT_ERR_ARG, "at most 32 ranks");
   if (!n || n[0] % nranks != 0 || n[1] % nranks != 0)
     return fail(JT_ERR_ARG, "n[0] and n[1] must be divisible by nranks");
   if (opts && opts->device == -2) return fail(JT_ERR_ARG, "distributed plans need a device");
@@ -1384,8 +1561,16 @@ static jt_status plan_dist_common(jt_plan_t *out, int d, const int64_t n[], cons
   }
   if (!(flags & JT_DIST_LOWMEM)) {
     const size_t bytes = (size_t)p->total * sizeof(double);
-    if (cudaMalloc((void **)&p->a2a_send, bytes) != cudaSuccess ||
-        cudaMalloc((void **)&p->a2a_recv, bytes) != cudaSuccess) {
+    if (cudaMalloc((void **)&p->a2a_recv, bytes) != cudaSuccess ||
+        (!group && cudaMalloc((void **)&p->bar_buf, sizeof(double)) != cudaSuccess)) {
+      jt_destroy(p);
+      return fail(JT_ERR_ALLOC, "all-to-all buffers");
+    }
+    if (!group) cudaMemset(p->bar_buf, 0, sizeof(double));
+    // the fused exchange unless the caller asks for the NCCL all-to-all: peer pointers to every rank's receive
+    // buffer (all ranks agree on the outcome: setup_ipc is collective and falls back for everyone)
+    if (!(flags & JT_DIST_NCCL_A2A)) p->p2p = group ? true : setup_ipc(p);
+    if (!p->p2p && cudaMalloc((void **)&p->a2a_send, bytes) != cudaSuccess) {
       jt_destroy(p);
       return fail(JT_ERR_ALLOC, "all-to-all buffers");
     }
@@ -1403,6 +1588,13 @@ jt_status jt_plan_dist_ex(jt_plan_t *out, int d, const int64_t n[], const double
                           const jt_opts *opts, const void *nccl_unique_id, int rank, int nranks, int flags) {
   if (!nccl_unique_id) return fail(JT_ERR_ARG, "null id");
   return plan_dist_common(out, d, n, a, b, eps, opts, rank, nranks, flags, nccl_unique_id, nullptr);
+}
+
+jt_status jt_dist_mode(jt_plan_t p, int *mode) {
+  if (!p || !mode) return fail(JT_ERR_ARG, "null argument");
+  *mode = !p->dist ? JT_MODE_SINGLE
+                   : (p->dist_flags & JT_DIST_LOWMEM) ? JT_MODE_LOWMEM : (p->p2p ? JT_MODE_FUSED : JT_MODE_A2A);
+  return JT_OK;
 }
 
 jt_status jt_sync(jt_plan_t p, void *cuda_stream) {

@@ -98,7 +98,7 @@ def distributed_cases():
     for G, shape, a, b in [(2, (64, 48, 40), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)),
                            (4, (96, 64, 33), (0.25, -0.1, 0.0), (-0.25, 0.6, 0.0)),
                            (4, (256, 256), (0.1, -0.25), (-0.4, 0.35))]:
-        for flags in (0, jt.JT_DIST_LOWMEM):
+        for flags in (0, jt.JT_DIST_LOWMEM, jt.JT_DIST_NCCL_A2A):
             g = jt.jt_debug_vgroup_create(G, 60000)
             plans = [LibSlabPlan(shape, a, b, 1e-12, vgroup=g, rank=r, flags=flags) for r in range(G)]
             streams = [torch.cuda.Stream() for _ in range(G)]

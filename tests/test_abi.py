@@ -120,7 +120,8 @@ def test_dist_and_debug_argument_errors():
     o.device = -2
     assert jt._lib.jt_plan_dist_ex(ctypes.byref(h), 2, n, a, a, 1e-12, ctypes.byref(o), uid, 0, 2, 0) == jt.JT_ERR_ARG
     o.device = -1
-    assert jt._lib.jt_plan_dist_ex(ctypes.byref(h), 2, n, a, a, 1e-12, ctypes.byref(o), uid, 0, 2, 2) == jt.JT_ERR_ARG
+    assert jt._lib.jt_plan_dist_ex(ctypes.byref(h), 2, n, a, a, 1e-12, ctypes.byref(o), uid, 0, 2, 4) == jt.JT_ERR_ARG
+    assert jt._lib.jt_plan_dist_ex(ctypes.byref(h), 2, n, a, a, 1e-12, ctypes.byref(o), uid, 0, 33, 0) == jt.JT_ERR_ARG
     assert jt._lib.jt_plan_dist_ex(ctypes.byref(h), 2, n, a, a, 1e-12, ctypes.byref(o), None, 0, 2, 0) == jt.JT_ERR_ARG
     with pytest.raises(jt.JTError):
         jt.jt_debug_vgroup_create(0)

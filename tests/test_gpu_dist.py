@@ -99,11 +99,16 @@ def gather_x(xs):
     return np.concatenate([x.cpu().numpy() for x in xs], axis=0)
 
 
+MODES = [0, 2]  # the fused exchange (default: blocks stored straight into the peers' receive buffers) and
+#                 JT_DIST_NCCL_A2A (the chunked all-to-all pipelined with the axis-1 pass; here the in-process copies)
+
+
+@pytest.mark.parametrize("flags", MODES)
 @pytest.mark.parametrize("world,shape,a,b", SHAPES)
-def test_library_slab_transform_virtual_ranks(world, shape, a, b):
-    """jt_forward / jt_inverse on G distributed plans (transform_dist: pipelined axis-1 pass + exchange in row chunks,
-    chunk-major layouts with ostride > outer) against the oracle; the round trip; repeat determinism."""
-    grp = Group(world, shape, a, b)
+def test_library_slab_transform_virtual_ranks(world, shape, a, b, flags):
+    """jt_forward / jt_inverse on G distributed plans (transform_dist: the fused exchange, or the pipelined axis-1 pass
+    + all-to-all in row chunks with ostride > outer) against the oracle; the round trip; repeat determinism."""
+    grp = Group(world, shape, a, b, flags=flags)
     try:
         x = si.gaussian(shape, seed=11)
         xs = x_slabs(grp, x)
@@ -127,13 +132,14 @@ def test_library_slab_transform_virtual_ranks(world, shape, a, b):
         grp.close()
 
 
+@pytest.mark.parametrize("flags", MODES)
 @pytest.mark.parametrize("world,shape,a,b", [SHAPES[1], SHAPES[4], SHAPES[6]])
-def test_library_slab_host_paths_virtual_ranks(world, shape, a, b):
+def test_library_slab_host_paths_virtual_ranks(world, shape, a, b, flags):
     """The distributed host-buffer paths: jt_forward_host (x-slab copied in row chunks feeding the local passes and
     the chunked exchange, y-slab copied back in column blocks), two jt_forward_host_async calls in flight through the
     staging slots, and jt_inverse_host, against the device-pointer path (equal up to rounding: a row chunk may take
     a term-split launch) and the oracle."""
-    grp = Group(world, shape, a, b)
+    grp = Group(world, shape, a, b, flags=flags)
     try:
         x = si.gaussian(shape, seed=21)
         xs = x_slabs(grp, x)
@@ -261,8 +267,8 @@ def test_lowmem_capacity_mode_virtual_ranks(world, shape, a, b):
 
 def test_lowmem_footprint():
     """Per-rank device memory of a capacity-mode plan: the plan's factors only (no slab-sized buffer), i.e. the
-    caller's two slabs + the factors (~0.1 MB per axis here) per GPU; the pipelined mode adds exactly its two
-    all-to-all slabs.  Measured with cudaMemGetInfo around plan creation and one forward per rank, at 256^3 over 2
+    caller's two slabs + the factors (~0.1 MB per axis here) per GPU; the fused-exchange mode adds one receive slab,
+    the NCCL all-to-all mode two (send + receive).  Measured with cudaMemGetInfo around plan creation and one forward per rank, at 256^3 over 2
     virtual ranks (64 MiB slabs), against G single-GPU plans of the same shape (the same factor allocations)."""
     shape, a, b, G = (256, 256, 256), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1), 2
     slab_bytes = 8 * int(np.prod(shape)) // G
@@ -293,9 +299,11 @@ def test_lowmem_footprint():
         return lambda: [p.close() for p in ps]
     base = measure(single_plans)
     lowmem = dist_group(jt.JT_DIST_LOWMEM)
-    plain = dist_group(0)
+    fused = dist_group(0)
+    a2a = dist_group(jt.JT_DIST_NCCL_A2A)
     assert lowmem - base <= 0.05 * G * slab_bytes, (lowmem, base, slab_bytes)
-    assert plain - lowmem >= 1.9 * G * slab_bytes, (plain, lowmem, slab_bytes)
+    assert 0.95 * G * slab_bytes <= fused - lowmem <= 1.05 * G * slab_bytes, (fused, lowmem, slab_bytes)
+    assert a2a - lowmem >= 1.9 * G * slab_bytes, (a2a, lowmem, slab_bytes)
 
 
 def test_virtual_exchange_failure_aborts():
@@ -362,7 +370,7 @@ def test_checks_build_parity_and_no_violations():
 
 
 @pytest.mark.parametrize("name,world,flags", [("cfg5_3d_512", 8, 0), ("cfg3_2d_4096", 8, 0), ("cfg4_3d_256", 4, 0),
-                                              ("cfg5_3d_512", 8, 1)])
+                                              ("cfg5_3d_512", 8, 1), ("cfg5_3d_512", 8, 2)])
 def test_full_size_distributed_virtual_ranks(name, world, flags):
     """The BASELINE multi-GPU configs at full size through the library's distributed schedule (the launch
     configuration bench.py runs under torchrun, G virtual ranks; flags 1 = JT_DIST_LOWMEM): the assembled y-slabs
