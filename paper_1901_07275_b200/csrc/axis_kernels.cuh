@@ -1242,6 +1242,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   cx.finish();
   if constexpr (TSPLIT && C::CLUSTER_FIT)
     if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n);
+  if constexpr (SPLIT)
+    if (lay.out_peer) __threadfence_system();  // (the fused exchange: this thread's peer stores performed system-wide)
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1525,6 +1527,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   cx.finish();
   if constexpr (TSPLIT && C::CLUSTER_FIT)
     if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n);
+  if constexpr (SPLIT)
+    if (lay.out_peer) __threadfence_system();  // (the fused exchange: this thread's peer stores performed system-wide)
 }
 
 }  // namespace jtk
