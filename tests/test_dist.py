@@ -5,9 +5,11 @@ logic: which local passes run, with which (outer, inner, split) geometry, and th
 the chunk-major blocks turns x-slabs into y-slabs (and back).  The composed result must equal the
 oracle's full transform restricted to this rank's box.
 
-The GPU kernels' handling of the same layouts is checked in tests/test_gpu.py
-(test_chunk_major_layouts_virtual_ranks) against the oracle, one GPU, virtual ranks run one after
-another (no kernel waits on another).
+The LIBRARY's own distributed schedule (transform_dist / the distributed host paths: the pipelined row-chunk
+launches with ostride > outer, the fused peer-store exchange and the NCCL all-to-all mode, capacity mode) runs at
+G = 2, 4, 8 virtual ranks on one GPU in tests/test_gpu_dist.py, against the oracle and bit for bit against this
+module's Python twin (dist.SlabPlan); tests/test_gpu.py::test_chunk_major_layouts_virtual_ranks covers the twin's
+whole-slab chunk-major launches (ostride == outer).
 """
 import os
 import socket
