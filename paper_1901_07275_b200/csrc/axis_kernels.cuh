@@ -550,6 +550,40 @@ __device__ __forceinline__ void pass_compute(double (&xr)[C::R], double (&xi)[C:
     }
 #pragma unroll
     for (int i = 0; i < P::B; ++i) dft<RS>(&xr[i * RS], &xi[i * RS]);
+  } else if constexpr (C::TWT && JT_TW_PREISSUE) {
+    // as below, but each chunk's TMEM loads are issued one chunk ahead, so the loads of butterfly i + 1's first chunk
+    // are in flight during butterfly i's DFT (one exposed TMEM latency per pass instead of one per chunk)
+    constexpr int NCHK = (RS - 1 + 7) / 8;
+    const uint32_t tb = ttw + 4 * TwPrefix<C::N, C::R, NS>::value;
+    double w[16];
+    tmem_ld_d8(tb, &w[0]);
+    tmem_ld_d8(tb + 16, &w[8]);
+#pragma unroll
+    for (int i = 0; i < P::B; ++i) {
+#pragma unroll
+      for (int ch = 0; ch < NCHK; ++ch) {
+        tmem_wait_ld();
+        double wc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) wc[j] = w[j];
+        if (ch + 1 < NCHK || i + 1 < P::B) {
+          const uint32_t tn = ch + 1 < NCHK ? tb + 4 * (i * (RS - 1)) + 32 * (ch + 1) : tb + 4 * ((i + 1) * (RS - 1));
+          tmem_ld_d8(tn, &w[0]);
+          tmem_ld_d8(tn + 16, &w[8]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = 1 + 8 * ch + j;
+          if (r < RS) {
+            const double pr = wc[2 * j], pim = wc[2 * j + 1];
+            const double tr = xr[i * RS + r] * pr - xi[i * RS + r] * pim;
+            xi[i * RS + r] = fma(xr[i * RS + r], pim, xi[i * RS + r] * pr);
+            xr[i * RS + r] = tr;
+          }
+        }
+      }
+      dft<RS>(&xr[i * RS], &xi[i * RS]);
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < P::B; ++i) {
@@ -924,29 +958,33 @@ struct Layout {
   long long ostride;  // outer extent of the chunk-major blocks (== outer, or the whole slab when a launch
                       // covers only part of its rows: the pipelined all-to-all of the distributed forward)
   long long in_lim, out_lim;  // elements readable / writable from the in / out pointers (JT_CHECKS builds)
-  // element offset of chunk-major block g from the in / out pointer (g < split): g ostride cs inner for one
-  // buffer, or (out_peer) the block's place in ANOTHER allocation -- rank g's receive buffer mapped over NVLink
-  // (CUDA IPC), so the pass stores each block straight into the peer that owns it (the fused slab exchange)
-  long long itab[MAX_SPLIT], otab[MAX_SPLIT];
-  int out_peer;
+  // out_peer != nullptr (chunk-major output only): block g of the output is NOT at g ostride cs inner from `out`
+  // but in ANOTHER allocation -- rank g's receive buffer mapped over NVLink (CUDA IPC) -- at element offset
+  // out_peer[g] + out_row from `out` (a plan-owned device array), so the pass stores each block straight into the
+  // peer that owns it (the fused slab exchange)
+  const long long *out_peer;
+  long long out_row;
 };
 
 
 // SPLIT is a template flag (a separate kernel instantiation) so that the plain layout costs no registers.
 template <bool SPLIT>
 struct LineAddr {
-  long long b0, inner;
+  long long b0, cstride, inner;
   int cs;
-  const long long *tab;  // Layout::itab / otab (kernel parameter space: the Layout is a __grid_constant__)
-  __device__ __forceinline__ LineAddr(long long L, const long long *tab_, long long inner_, int n, int cs_) {
+  const long long *peer;  // Layout::out_peer (output side of a fused-exchange pass), else nullptr
+  __device__ __forceinline__ LineAddr(long long L, long long outer, long long inner_, int n, int cs_,
+                                      const long long *peer_ = nullptr, long long row = 0) {
     const long long o = L / inner_, i = L - o * inner_;
     inner = inner_;
     cs = SPLIT ? cs_ : n;
-    b0 = o * (long long)cs * inner_ + i;
-    tab = tab_;
+    b0 = o * (long long)cs * inner_ + i + (SPLIT && peer_ ? row : 0);
+    cstride = SPLIT ? outer * (long long)cs * inner_ : 0;  // outer = Layout::ostride (see the kernels)
+    peer = SPLIT ? peer_ : nullptr;
   }
   __device__ __forceinline__ long long at(int j) const {
-    if constexpr (SPLIT) return b0 + tab[j / cs] + (long long)(j % cs) * inner;
+    if constexpr (SPLIT)
+      return b0 + (peer ? __ldg(&peer[j / cs]) : (long long)(j / cs) * cstride) + (long long)(j % cs) * inner;
     else return b0 + (long long)j * inner;
   }
 };
@@ -961,7 +999,7 @@ __device__ __forceinline__ void prefetch_next_line(const double *in, const Layou
     if (L >= nlines) return;
     const bool mine = lay.inner == 1 ? (vt % 16 == 0) : (lay.inner % 16 == 0 ? (L % 16 == 0) : true);
     if (!mine) return;
-    const LineAddr<SPLIT> ia(L, lay.itab, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> ia(L, lay.ostride, lay.inner, n, lay.in_cs);
 #pragma unroll
     for (int r = 0; r < C::R; ++r) {
       const int k = vt + r * C::TPL;
@@ -1015,8 +1053,7 @@ __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts,
 // ------------------------------------------------------------------------------------------------
 template <class C, bool SPLIT, bool TSPLIT = false>
 __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, const __grid_constant__ Layout lay,
-                                                             TermSplit ts) {
+                                                             long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
@@ -1034,8 +1071,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr<SPLIT> ia(live ? L : 0, lay.itab, lay.inner, n, lay.in_cs);
-    const LineAddr<SPLIT> oa(live ? L : 0, lay.otab, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs, lay.out_peer, lay.out_row);
 
     // coefficients at the first-pass input positions k = vt + r TPL; degrees < k0 also to alow
     // (all loads issued before any shared-memory store, so that their latencies overlap)
@@ -1251,8 +1288,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 // ------------------------------------------------------------------------------------------------
 template <class C, bool SPLIT, bool TSPLIT = false>
 __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const double *in, double *out,
-                                                             long long nlines, const __grid_constant__ Layout lay,
-                                                             TermSplit ts) {
+                                                             long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
   Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
@@ -1272,8 +1308,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
     const long long L = (bt * C::GPC + cx.grp) * LG + line;
     const bool live = L < nlines;
-    const LineAddr<SPLIT> ia(live ? L : 0, lay.itab, lay.inner, n, lay.in_cs);
-    const LineAddr<SPLIT> oa(live ? L : 0, lay.otab, lay.inner, n, lay.out_cs);
+    const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
+    const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs, lay.out_peer, lay.out_row);
 
     State<C, NB * MAXR> yb(cx.priv, cx.gt, cx.taddr);  // element q MAXR + c: row c of input bin q
     {

@@ -231,6 +231,11 @@ struct jt_plan_s {
   bool p2p = false;
   double *peer_recv[jtk::MAX_SPLIT] = {};
   bool peer_ipc[jtk::MAX_SPLIT] = {};  // peer_recv[g] was opened with cudaIpcOpenMemHandle (closed at destroy)
+  // element offsets (from this rank's receive buffer) of block `rank` in every rank's receive buffer, on the host
+  // and (read by the kernels' chunk-major output addressing) on the device; set by resolve_peers
+  long long h_peer_off[jtk::MAX_SPLIT] = {};
+  long long *d_peer_off = nullptr;
+  bool peers_resolved = false;
   double *bar_buf = nullptr;           // one double for the NCCL barrier (an all-reduce)
   mutable cudaStream_t s_comm = nullptr;  // the pipelined all-to-all's stream (created on first use)
   mutable cudaEvent_t ev_chunk[8] = {}, ev_comm = nullptr;
@@ -465,13 +470,13 @@ jt_status launch_n(const jt_plan_s *p, bool inverse, int maxr, const jtk::AxisDe
 // One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
 // layout of the slab all-to-all for the input / output.
 // in_lim / out_lim: elements of the input / output buffers from the given pointers (bounds of the JT_CHECKS
-// build; -1: the extent the geometry addresses).  peer_off: out_split element offsets of the output blocks from
-// `out` when they live in other allocations (the fused slab exchange: each block stored into its rank's receive
-// buffer over NVLink); nullptr: one buffer, block g at g ostride (n / out_split) inner.
+// build; -1: the extent the geometry addresses).  peer: the fused slab exchange -- the out_split output blocks
+// live in the ranks' receive buffers, at the plan's peer offsets (from `out` = this rank's receive buffer) + the
+// row offset peer_row; false: one buffer, block g at g ostride (n / out_split) inner.
 jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *in, double *out, long long outer,
                       long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
                       long long nlines_only = -1, bool allow_ts = true, long long ostride = -1,
-                      long long in_lim = -1, long long out_lim = -1, const long long *peer_off = nullptr) {
+                      long long in_lim = -1, long long out_lim = -1, bool peer = false, long long peer_row = 0) {
   jtk::AxisDev ax = axis_dev(p, axis);
   const int maxr = p->dev[axis].maxr;
   // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
@@ -479,24 +484,13 @@ jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *
   const long long ost = ostride >= 0 ? ostride : outer;
   const long long n = p->n[axis];
   const long long geo_in = (in_split > 1 ? ost : outer) * n * inner, geo_out = (out_split > 1 ? ost : outer) * n * inner;
-  if (in_split > jtk::MAX_SPLIT || out_split > jtk::MAX_SPLIT) return fail(JT_ERR_ARG, "in_split / out_split > 32");
-  if (peer_off && out_split == 1) {  // one block (a world of one): the plain layout at that block's place
-    out += peer_off[0];
-    peer_off = nullptr;
+  if (peer && out_split == 1) {  // one block (a world of one): the plain layout at that block's place
+    out += p->h_peer_off[0] + peer_row;
+    peer = false;
   }
-  jtk::Layout lay;
-  lay.outer = outer;
-  lay.inner = inner;
-  lay.in_cs = (int)(n / in_split);
-  lay.out_cs = (int)(n / out_split);
-  lay.ostride = ost;
-  lay.in_lim = in_lim >= 0 ? in_lim : geo_in;
-  lay.out_lim = out_lim >= 0 ? out_lim : geo_out;
-  for (int g = 0; g < jtk::MAX_SPLIT; ++g) {
-    lay.itab[g] = g < in_split ? g * ost * lay.in_cs * inner : 0;
-    lay.otab[g] = g < out_split ? (peer_off ? peer_off[g] : g * ost * lay.out_cs * inner) : 0;
-  }
-  lay.out_peer = peer_off != nullptr;
+  const jtk::Layout lay{outer, inner, (int)(n / in_split), (int)(n / out_split), ost,
+                        in_lim >= 0 ? in_lim : geo_in, out_lim >= 0 ? out_lim : geo_out,
+                        peer ? p->d_peer_off : nullptr, peer ? peer_row : 0};
   switch (ax.N) {
     case 16: return launch_n<16>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
     case 32: return launch_n<32>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
@@ -550,6 +544,8 @@ void free_device(jt_plan_s *p) {
     if (p->peer_ipc[g]) cudaIpcCloseMemHandle(p->peer_recv[g]), p->peer_ipc[g] = false;
   cudaFree(p->bar_buf);
   p->bar_buf = nullptr;
+  cudaFree(p->d_peer_off);
+  p->d_peer_off = nullptr;
   cudaFree(p->a2a_send);
   cudaFree(p->a2a_recv);
   p->a2a_send = p->a2a_recv = nullptr;
@@ -794,10 +790,12 @@ jt_status dist_barrier(const jt_plan_s *p, cudaStream_t s) {
   return poll_comm(p);
 }
 
-// Offsets (elements, from this rank's receive buffer, the launch's `out`) of the blocks this rank stores into each
-// rank's receive buffer: block `rank` of rank g's buffer, rows from `rowoff`.  The virtual group resolves its
-// members' buffers here (they exist once every member's plan is built).
-jt_status peer_offsets(const jt_plan_s *p, long long rowoff, long long off[]) {
+// The fused exchange's block offsets (h_peer_off / d_peer_off): block `rank` of rank g's receive buffer, in elements
+// from this rank's receive buffer (the launches' `out`).  Computed once; the virtual group resolves its members'
+// buffers here (they exist once every member's plan is built), the NCCL plans from the IPC-mapped pointers.
+jt_status resolve_peers(const jt_plan_s *p, cudaStream_t s) {
+  if (p->peers_resolved) return JT_OK;
+  jt_plan_s *q = const_cast<jt_plan_s *>(p);
   const long long chunk = p->total / p->nranks;
   for (int g = 0; g < p->nranks; ++g) {
     const double *base = p->peer_recv[g];
@@ -806,8 +804,13 @@ jt_status peer_offsets(const jt_plan_s *p, long long rowoff, long long off[]) {
       base = p->vgroup->member[g] ? p->vgroup->member[g]->a2a_recv : nullptr;
     }
     if (!base) return fail(JT_ERR_ARG, "fused exchange: rank " + std::to_string(g) + " has no plan yet");
-    off[g] = (long long)(base - p->a2a_recv) + p->rank * chunk + rowoff;
+    q->h_peer_off[g] = (long long)(base - p->a2a_recv) + p->rank * chunk;
   }
+  if (!q->d_peer_off && cudaMalloc((void **)&q->d_peer_off, jtk::MAX_SPLIT * sizeof(long long)) != cudaSuccess)
+    return fail(JT_ERR_ALLOC, "peer offsets");
+  JT_CUDA_TRY(cudaMemcpyAsync(q->d_peer_off, q->h_peer_off, jtk::MAX_SPLIT * sizeof(long long), cudaMemcpyHostToDevice, s));
+  JT_CUDA_TRY(cudaStreamSynchronize(s));  // (h_peer_off is the source: keep it alive and the copy done)
+  q->peers_resolved = true;
   return JT_OK;
 }
 
@@ -854,8 +857,7 @@ jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, dou
   if (p->p2p) {
     // fused exchange: the pass before it stores every chunk-major block straight into the receive buffer of the rank
     // that owns it (over NVLink), so the transfer overlaps the pass line by line; two barriers bracket it
-    long long off[jtk::MAX_SPLIT];
-    if ((st = peer_offsets(p, 0, off)) != JT_OK) return st;
+    if ((st = resolve_peers(p, s)) != JT_OK) return st;
     if (d == 3) {
       if ((st = mark(p, PM_AX + 4, s)) != JT_OK) return st;
       if ((st = launch_axis(p, 2, inverse, in, out, inverse ? n0 * c : R * n1, 1, s)) != JT_OK) return st;
@@ -865,8 +867,8 @@ jt_status transform_dist(const jt_plan_s *p, bool inverse, const double *in, dou
     if ((st = dist_barrier(p, s)) != JT_OK) return st;  // the peers are done reading their receive buffers
     const int ax1 = inverse ? 0 : 1, ax2 = inverse ? 1 : 0;
     if ((st = mark(p, PM_AX + 2 * ax1, s)) != JT_OK) return st;
-    if (inverse) st = launch_axis(p, 0, true, src, p->a2a_recv, 1, c * r, s, 1, G, -1, true, -1, -1, -1, off);
-    else st = launch_axis(p, 1, false, src, p->a2a_recv, R, r, s, 1, G, -1, true, -1, -1, -1, off);
+    if (inverse) st = launch_axis(p, 0, true, src, p->a2a_recv, 1, c * r, s, 1, G, -1, true, -1, -1, -1, true, 0);
+    else st = launch_axis(p, 1, false, src, p->a2a_recv, R, r, s, 1, G, -1, true, -1, -1, -1, true, 0);
     if (st != JT_OK) return st;
     if ((st = mark(p, PM_AX + 2 * ax1 + 1, s)) != JT_OK) return st;
     if ((st = mark(p, PM_XS, s)) != JT_OK) return st;
@@ -1064,10 +1066,9 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
         src1 = sout + off;
       }
       if (p->p2p) {  // this chunk's rows of every block straight into their owners' receive buffers
-        long long poff[jtk::MAX_SPLIT];
-        if ((st = peer_offsets(p, r0 * c * r, poff)) != JT_OK) return st;
+        if ((st = resolve_peers(p, s)) != JT_OK) return st;
         if ((st = launch_axis(p, 1, false, src1, p->a2a_recv, r1 - r0, r, s, 1, G, -1, true, R,
-                              p->total - (long long)off, -1, poff)) != JT_OK)
+                              p->total - (long long)off, -1, true, r0 * c * r)) != JT_OK)
           return st;
         continue;
       }
@@ -1120,10 +1121,9 @@ jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double 
         return st;
     }
     if (p->p2p) {  // the axis-0 pass stores every block straight into its owner's receive buffer
-      long long poff[jtk::MAX_SPLIT];
-      if ((st = peer_offsets(p, 0, poff)) != JT_OK) return st;
+      if ((st = resolve_peers(p, s)) != JT_OK) return st;
       if ((st = launch_axis(p, 0, true, d == 3 ? sout : sin, p->a2a_recv, 1, yrow, s, 1, G, -1, true, -1, -1, -1,
-                            poff)) != JT_OK)
+                            true, 0)) != JT_OK)
         return st;
       if ((st = dist_barrier(p, s)) != JT_OK) return st;  // every rank's blocks have landed here
     } else {
