@@ -34,7 +34,7 @@
 #define JT_TWT 1  // per-thread twiddles in TMEM (N <= 1024: 512^3 forward 17.9 -> 17.3 ms)
 #endif
 #ifndef JT_TW_PREISSUE
-#define JT_TW_PREISSUE 0  // TMEM twiddle chunks loaded one chunk ahead (the next butterfly's during the DFT)
+#define JT_TW_PREISSUE 0  // TMEM twiddle chunks loaded one chunk ahead (the next butterfly's during the DFT; r02v: no change)
 #endif
 #ifndef JT_TWT_INV32
 #define JT_TWT_INV32 0  // ... also for the radix-32 inverse (measured 2 % slower)
