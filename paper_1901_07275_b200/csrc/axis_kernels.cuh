@@ -256,6 +256,12 @@ struct Cfg {
   // (tools/ab_time.py, r02i): N = 4096 forward (no ring) 3.54 -> 3.45 ms at 4096^2; everywhere else slower (the
   // per-warp ring releases cost more than the barrier: 512^3 +3.8 %, 4096 inverse +6 %), so only there.
   static constexpr bool LATE = JT_LATE_SYNC && !SUB && !INV && !STAGED && !URING_WANT;
+  // forward column scale folded into the radix-32 first pass's first butterfly layer (fft_regs.cuh dft4_pre): 32 fewer
+  // FP64 instructions per thread and term; measured (r02x) 4096^2 forward 3.46 -> 3.37 ms, but 512^3 +0.75 %, 1024
+  // +1.2 %, 128 +1.6 % (the MUL -> FMA chain lengthens the dependent path), so only for N >= JT_A1_FOLD_NMIN
+  static constexpr bool A1FOLD = JT_A1_FOLD && N >= JT_A1_FOLD_NMIN && !INV && R == 32 && Pass<N, R, 1>::RS == 32 &&
+                                 Pass<N, R, 1>::B == 1 &&
+                                 PRIV && !SUB && (!(JT_LOADS_FIRST & 1) || STAGED || !TPRIV);
   static constexpr bool URING = URING_WANT && GPC * GROUP_BYTES + hdr_bytes(1) <= SMEM_LIMIT;
   static constexpr int sub_fit(int s) { return (s > 4 && GPC * GROUP_BYTES + hdr_bytes(s) > SMEM_LIMIT) ? sub_fit(s - 1) : s; }
   // a third ring stage when it fits next to the GPC groups; SUB: as many sub-stages as fit (<= one term)
@@ -703,12 +709,13 @@ __device__ __forceinline__ void run_passes(double (&xr)[C::R], double (&xi)[C::R
 
 // Full FFT of one term; first-pass inputs (positions vt + r TPL) in registers on entry, last-pass
 // outputs (positions out_pos) in registers on exit.  The caller syncs the group before the next call.
-template <class C>
+template <class C, bool PRE = false>
 __device__ __forceinline__ void fft(double (&xr)[C::R], double (&xi)[C::R], void *buf, int vt, int line,
                                     const double2 *__restrict__ tw, uint32_t ttw) {
   using P0 = Pass<C::N, C::R, 1>;
+  static_assert(!PRE || (P0::RS == 32 && P0::B == 1), "PRE: one radix-32 first pass");
 #pragma unroll
-  for (int i = 0; i < P0::B; ++i) dft<P0::RS>(&xr[i * P0::RS], &xi[i * P0::RS]);
+  for (int i = 0; i < P0::B; ++i) dft<P0::RS, PRE>(&xr[i * P0::RS], &xi[i * P0::RS]);
   if constexpr (!P0::LAST) {
     if constexpr (C::LATE) group_sync<C>();  // every thread of the group has read the previous term's exchange
     do_exchange<C, 1>(xr, xi, buf, vt, line);
@@ -1181,6 +1188,27 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
             }
           }
         }
+      } else if constexpr (C::A1FOLD) {
+        // A1 folded into the first butterfly layer of the radix-32 DFT: positions r < 16 scaled (state chunk 0), then
+        // x_r +- x_{r+16} = fma(+-v_{r+16}, a_{r+16}, v_r a_r) with state chunk 1 (dft<32, true> skips that layer)
+        double ac[State<C, R>::CH];
+        a.chunk(0, ac);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double2 vv = vl[vt + r * TPL];
+          xr[r] = vv.x * ac[r];
+          xi[r] = vv.y * ac[r];
+        }
+        a.chunk(1, ac);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double2 vv = vl[vt + (r + 16) * TPL];
+          const double tr = xr[r], ti = xi[r];
+          xr[r] = fma(vv.x, ac[r], tr);
+          xi[r] = fma(vv.y, ac[r], ti);
+          xr[r + 16] = fma(-vv.x, ac[r], tr);
+          xi[r + 16] = fma(-vv.y, ac[r], ti);
+        }
       } else {
 #pragma unroll
         for (int ch = 0; ch < State<C, R>::NCH; ++ch) {  // A1
@@ -1204,7 +1232,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
           for (int c = 0; c < MAXR; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(ul + c * NBINS + m[q]));
       }
-      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // A2
+      fft<C, C::A1FOLD>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // A2
       cx.acquire_u(seq);
       if constexpr (C::SUB) {
         // A3 from the ring: sub-stage 4 + i holds rows c of bins h 1024 + 256 i + [0, 256), i.e. the thread's bins

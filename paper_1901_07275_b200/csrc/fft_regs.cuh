@@ -66,12 +66,23 @@ JT_DEV void dft4(double *xr, double *xi) {
   xr[3] = t1r + t3i; xi[3] = t1i - t3r;  // t1 - i t3
 }
 
-template <int M>
+// dft4 whose first butterfly layer is already applied: inputs (x0 + x2, x1 + x3, x0 - x2, x1 - x3).
+JT_DEV void dft4_pre(double *xr, double *xi) {
+  const double t0r = xr[0], t0i = xi[0], t2r = xr[1], t2i = xi[1], t1r = xr[2], t1i = xi[2], t3r = xr[3], t3i = xi[3];
+  xr[0] = t0r + t2r; xi[0] = t0i + t2i;
+  xr[2] = t0r - t2r; xi[2] = t0i - t2i;
+  xr[1] = t1r - t3i; xi[1] = t1i + t3r;
+  xr[3] = t1r + t3i; xi[3] = t1i - t3r;
+}
+
+template <int M, bool PRE = false>
 JT_DEV void dft(double *xr, double *xi);
 
 // Cooley-Tukey M = N1 N2 in registers: n = N2 n1 + n2, k = k1 + N1 k2.
 //   Y[k1][n2] = DFT_N1 over n1 of x[N2 n1 + n2];  Y *= w_M^{n2 k1};  X[k1 + N1 k2] = DFT_N2 over n2.
-template <int N1, int N2>
+// PRE (N1 = 4): the inputs already hold the first butterfly layer of the DFT_4s, x[n] +- x[n + M/2] at n and
+// n + M/2 (n < M/2) -- the forward's column scale computes them with FMAs (dft<32, true>).
+template <int N1, int N2, bool PRE = false>
 JT_DEV void dft_ct(double *xr, double *xi) {
   constexpr int M = N1 * N2;
   double yr[M], yi[M];
@@ -80,7 +91,12 @@ JT_DEV void dft_ct(double *xr, double *xi) {
     double ar[N1], ai[N1];
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) { ar[n1] = xr[N2 * n1 + n2]; ai[n1] = xi[N2 * n1 + n2]; }
-    dft<N1>(ar, ai);
+    if constexpr (PRE) {
+      static_assert(N1 == 4, "PRE: first layer of DFT_4");
+      dft4_pre(ar, ai);
+    } else {
+      dft<N1>(ar, ai);
+    }
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) {
       twc<M>(n2 * k1, ar[k1], ai[k1]);
@@ -99,8 +115,9 @@ JT_DEV void dft_ct(double *xr, double *xi) {
   }
 }
 
-template <int M>
+template <int M, bool PRE>
 JT_DEV void dft(double *xr, double *xi) {
+  static_assert(!PRE || M == 32, "PRE: radix 32 only");
   if constexpr (M == 1) {
   } else if constexpr (M == 2) {
     dft2(xr, xi);
@@ -111,7 +128,7 @@ JT_DEV void dft(double *xr, double *xi) {
   } else if constexpr (M == 16) {
     dft_ct<4, 4>(xr, xi);
   } else if constexpr (M == 32) {
-    dft_ct<4, 8>(xr, xi);
+    dft_ct<4, 8, PRE>(xr, xi);
   } else {
     static_assert(M <= 32, "radix too large");
   }
