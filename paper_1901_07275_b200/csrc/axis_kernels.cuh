@@ -92,6 +92,21 @@ __device__ __forceinline__ bool chk(bool ok, int line) {
 #else
 #define JT_CHK(cond) true
 #endif
+// Schedule fuzzing (checks build only): before every synchronisation point (group barriers, ring waits and releases,
+// cluster barriers) a thread sometimes sleeps for up to ~1 us, so warps reach shared data in orders the normal build
+// rarely produces; a missing barrier then shows up as a parity failure or as two runs that differ (the checks test
+// runs every case twice and compares the bits).
+#ifndef JT_JITTER
+#define JT_JITTER JT_CHECKS
+#endif
+__device__ __forceinline__ void jitter() {
+#if JT_JITTER
+  unsigned t = (unsigned)clock64() * 2654435761u + threadIdx.x * 40503u + blockIdx.x * 977u;
+  t ^= t >> 13;
+  if ((t & 7u) == 0u) __nanosleep(t & 1023u);
+  __syncwarp();
+#endif
+}
 
 constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
 constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
@@ -309,11 +324,15 @@ __device__ __forceinline__ const double2 *tw_smem_base(int off) {
 
 template <class C>
 __device__ __forceinline__ void group_sync() {
+  jitter();
   if constexpr (C::GW == 1) {
     __syncwarp();
   } else {
     // non-.aligned form: correct even if a warp arrives diverged (PTX ISA, barrier.sync)
     asm volatile("barrier.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / C::GT)), "r"(C::GT) : "memory");
+    // the threads a non-aligned barrier releases need not run converged: reconverge before the warp-collective
+    // (.sync.aligned) tcgen05 loads that may follow (found by the checks build's schedule fuzzing)
+    __syncwarp();
   }
 }
 
@@ -426,12 +445,14 @@ struct Ring {
     }
   }
   __device__ __forceinline__ void wait_full(long long seq) const {
+    jitter();
     mbar_wait(&full[seq % C::NSTAGE], (uint32_t)((seq / C::NSTAGE) & 1));
     __syncwarp();  // lanes may leave the try_wait loop in different iterations: reconverge
   }
   // SUB: every warp releases each sub-stage once its lanes' values are in registers; the last of the CTA's warps
   // refills the slot with sub-stage seq + NSTAGE (same acq_rel counter / proxy fence protocol as release()).
   __device__ __forceinline__ void release_warp(long long seq) const {
+    jitter();
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
       const int s = (int)(seq % C::NSTAGE);
@@ -456,6 +477,7 @@ struct Ring {
   // increment, the refill after the last one; the proxy fence orders those generic-proxy reads before
   // the async-proxy (TMA) writes of the refill.
   __device__ __forceinline__ void release(long long seq, int gt) const {
+    jitter();
     if (gt == 0) {
       const int s = (int)(seq % C::NSTAGE);
       unsigned old;
@@ -1029,6 +1051,8 @@ __device__ __forceinline__ double *cluster_part() {
 template <class C>
 __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts, const Layout &lay, long long nlines,
                                                int n) {
+  jitter();
+  __syncwarp();  // (the cluster barrier is .aligned: the warp reconverges after the jitter)
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   unsigned rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));

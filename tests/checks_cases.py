@@ -1,6 +1,7 @@
 """Run by tests/test_gpu_dist.py::test_checks_build_parity_and_no_violations with JT_LIB = libjt_checks.so (the
-bounds-checked build, include/jt_debug.h jt_debug_checks): small cases of every kernel family and schedule against
-the oracle, then the violation counter must read zero; finally the negative control.  Prints "CHECKS OK"."""
+bounds-checked, schedule-fuzzed build, include/jt_debug.h jt_debug_checks): small cases of every kernel family and
+schedule against the oracle, each single-GPU case twice (bitwise equal: the fuzzed schedules expose races), then the
+violation counter must read zero; finally the negative control.  Prints "CHECKS OK"."""
 import os
 import sys
 import threading
@@ -48,8 +49,12 @@ def single_gpu_cases():
     for shape, a, b in cases:
         p = jt.Plan(shape, a, b, 1e-12)
         x = si.gaussian(shape, seed=7)
-        assert relerr(dev(p, x), oracle.forward(x, a, b)) <= TOL, shape
-        assert relerr(dev(p, x, inverse=True), oracle.inverse(x, a, b)) <= TOL, shape
+        y1, y2 = dev(p, x), dev(p, x)  # (the checks build fuzzes the schedule: a race makes the two runs differ)
+        assert np.array_equal(y1, y2), f"forward {shape}: two runs differ"
+        assert relerr(y1, oracle.forward(x, a, b)) <= TOL, shape
+        z1, z2 = dev(p, x, inverse=True), dev(p, x, inverse=True)
+        assert np.array_equal(z1, z2), f"inverse {shape}: two runs differ"
+        assert relerr(z1, oracle.inverse(x, a, b)) <= TOL, shape
         if len(shape) >= 2:  # the pipelined host paths (row chunks, column blocks)
             assert relerr(p.forward_host(x), oracle.forward(x, a, b)) <= TOL, shape
             assert relerr(p.inverse_host(x), oracle.inverse(x, a, b)) <= TOL, shape
