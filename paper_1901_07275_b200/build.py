@@ -30,36 +30,53 @@ def _run(cmd):
     subprocess.run(cmd, check=True)
 
 
-def _run_parallel(cmds):
-    procs = []
-    for cmd in cmds:
-        print("+", " ".join(cmd), flush=True)
-        procs.append((cmd, subprocess.Popen(cmd)))
-    for cmd, p in procs:
+def _run_parallel(cmds, jobs=None):
+    """Run the commands, at most `jobs` (default: CPU count) at a time."""
+    jobs = jobs or os.cpu_count() or 4
+    pending, running = list(cmds), []
+    while pending or running:
+        while pending and len(running) < jobs:
+            cmd = pending.pop(0)
+            print("+", " ".join(cmd), flush=True)
+            running.append((cmd, subprocess.Popen(cmd)))
+        cmd, p = running.pop(0)
         if p.wait() != 0:
+            for _, q in running:
+                q.kill()
             raise subprocess.CalledProcessError(p.returncode, cmd)
+
+
+# translation units of the CUDA side: the C ABI (jt_api.cu) and one unit per FFT length (launch_<N>.cu: that
+# length's kernel instantiations), largest first so the parallel compile ends sooner
+UNITS = ["launch_4096", "launch_512", "launch_2048", "launch_1024", "launch_256", "launch_128", "launch_64",
+         "launch_32", "launch_16", "jt_api"]
 
 
 def build(verbose_ptxas: bool = False, out: str = LIB, defines=(), tag: str = "", checks: bool = True) -> str:
     """Compile libjt.so (or a variant: `out` path, extra -D `defines`, object-file `tag`); with `checks` (default,
-    only for the default build) also libjt_checks.so, compiled in parallel."""
+    only for the default build) also libjt_checks.so.  All translation units compile in parallel."""
     nvcc = _nvcc()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     build_dir = os.path.join(HERE, "_build")
     os.makedirs(build_dir, exist_ok=True)
     plan_o = os.path.join(build_dir, "plan.o")
-    _run(["g++", "-std=c++17", "-O2", "-fPIC", "-fopenmp", *inc, "-c", os.path.join(CSRC, "plan.cpp"),
-          "-o", plan_o])
     base = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", *inc]
     if verbose_ptxas:
         base += ["-Xptxas", "-v"]
-    api_o = os.path.join(build_dir, f"jt_api{tag}.o")
-    jobs = [(out, api_o, [f"-D{d}" for d in defines])]
+    variants = [(out, tag, [f"-D{d}" for d in defines])]
     if checks and out == LIB and not defines:
-        jobs.append((LIB_CHECKS, os.path.join(build_dir, "jt_api_checks.o"), ["-DJT_CHECKS=1"]))
-    _run_parallel([[nvcc, *base, *dfl, "-c", os.path.join(CSRC, "jt_api.cu"), "-o", obj] for _, obj, dfl in jobs])
-    for lib, obj, _ in jobs:
-        _run([nvcc, *ARCH, "-shared", "-o", lib, obj, plan_o, "-Xcompiler", "-fopenmp", "-lgomp"])
+        variants.append((LIB_CHECKS, "_checks", ["-DJT_CHECKS=1"]))
+    cmds = [["g++", "-std=c++17", "-O2", "-fPIC", "-fopenmp", *inc, "-c", os.path.join(CSRC, "plan.cpp"), "-o", plan_o]]
+    objs = {}
+    for lib, tg, dfl in variants:
+        objs[lib] = []
+        for u in UNITS:
+            obj = os.path.join(build_dir, f"{u}{tg}.o")
+            objs[lib].append(obj)
+            cmds.append([nvcc, *base, *dfl, "-c", os.path.join(CSRC, f"{u}.cu"), "-o", obj])
+    _run_parallel(cmds)
+    for lib, _, _ in variants:
+        _run([nvcc, *ARCH, "-shared", "-o", lib, *objs[lib], plan_o, "-Xcompiler", "-fopenmp", "-lgomp"])
     return out
 
 

@@ -81,8 +81,10 @@ struct TermSplit {
 #ifndef JT_CHECKS
 #define JT_CHECKS 0
 #endif
-__device__ unsigned long long jt_check_count;
-__device__ int jt_check_line;
+// (static: one copy per translation unit / device module -- the launch_<N>.cu units each own one, summed by
+// jt_debug_checks through jtl::checks_io<N>)
+static __device__ unsigned long long jt_check_count;
+static __device__ int jt_check_line;
 __device__ __forceinline__ bool chk(bool ok, int line) {
   if (!ok && atomicAdd(&jt_check_count, 1ull) == 0ull) jt_check_line = line;
   return ok;
@@ -107,6 +109,49 @@ __device__ __forceinline__ void jitter() {
   __syncwarp();
 #endif
 }
+
+// Phase trace (dev builds only, -DJT_PHASES=1, tools/phases.py): thread 0 of every CTA records clock64 at the
+// phase boundaries of its first batch and prints them with the kernel's globaltimer start / end, so the critical
+// path of the latency-bound launches (configs 1-2) can be split into prologue, loads, terms and reduction.
+#ifndef JT_PHASES
+#define JT_PHASES 0
+#endif
+struct Phases {
+#if JT_PHASES
+  long long t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long g0 = 0;
+  __device__ __forceinline__ Phases() {
+    if (threadIdx.x == 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+      t[0] = clock64();
+    }
+  }
+  __device__ __forceinline__ void mark(int i, bool on = true) {
+    if (threadIdx.x == 0 && on && t[i] == 0) t[i] = clock64();
+  }
+  __device__ __forceinline__ void print(int kind, int n, int terms, long long inner) {
+    if (threadIdx.x == 0) {
+      unsigned long long g1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+      const long long e = clock64();
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      printf("PH k%d_i%lld n%d cta%d sm%u terms%d g0 %llu g1 %llu d %lld %lld %lld %lld %lld %lld %lld %lld\n", kind, inner,
+             n, (int)blockIdx.x, smid, terms, g0, g1, t[1] - t[0], t[2] - t[0], t[3] - t[0], t[4] - t[0], t[5] - t[0],
+             t[6] - t[0], t[7] - t[0], e - t[0]);
+    }
+  }
+#else
+  __device__ __forceinline__ void mark(int, bool = true) {}
+  __device__ __forceinline__ void print(int, int, int, long long) {}
+#endif
+};
+
+// Programmatic dependent launch (JT_PDL, launch.cuh launch_axis_kernel): every axis kernel lets the next kernel of
+// the stream launch at once (its CTAs are placed as this one's exit) and waits for the previous kernel's completion
+// and memory before its first access to the arrays; without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
 constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
@@ -771,6 +816,12 @@ struct Ctx {
   Ring<C> ring;
   long long nbatch, bt0, btstep;
   int slice = 0, S = 1, l0 = 0, l1 = 0;
+  // Group term split (term-split cluster launches whose batch fits in one group's LG lines, e.g. a 1D transform):
+  // the CTA's terms are dealt round-robin to gsl groups, which all process the lines of group 0 (lgrp) and keep
+  // separate partials (summed by cluster_reduce); groups grp >= gsl, and groups whose lines are all past the end
+  // (dead), only take part in the factor ring.
+  int gsl = 1, lgrp = 0;
+  bool dead = false;
   const double2 *gv, *gu;
   __device__ __forceinline__ Ctx(char *smem, const AxisDev &ax, long long nlines, const TermSplit &ts) {
     grp = threadIdx.x / C::GT;
@@ -810,6 +861,14 @@ struct Ctx {
       l1 = ax.r;
       mine = blockIdx.x < nbatch ? (nbatch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     }
+    lgrp = grp;
+    if (TSPLIT && ts.cluster && JT_GSPLIT && C::GPC > 1) {
+      const long long lines_b = nlines - bt0 * C::GPC * C::LG;
+      if (lines_b <= C::LG) gsl = min(min(C::GPC, JT_GSPLIT), max(l1 - l0, 1));
+      if (gsl > 1) lgrp = 0;
+    }
+    // (term-split launches only: one batch per CTA; the persistent launches keep the plain loop)
+    dead = TSPLIT && ((gsl > 1 && grp >= gsl) || (gsl == 1 && (bt0 * C::GPC + grp) * C::LG >= nlines));
     ring.l0 = l0;
     ring.rs = l1 - l0 > 0 ? l1 - l0 : 1;
     ring.total = mine * (l1 - l0) * (C::SUB ? C::NSUB : 1);
@@ -895,6 +954,25 @@ struct Ctx {
       __syncthreads();
       if (threadIdx.x < 32) tmem_dealloc(tbase, C::TALLOC);
     }
+  }
+  // Degrees [kv0, kv1) of the dense block's batch-start part [kin, k0) handled by this CTA: all of them, or (term
+  // split) this slice's share -- the partials of every slice are summed anyway, so the block need not wait on one CTA
+  // (slice 0 alone: 10 us of the 20 us 1D n = 1024 forward, tools/phases.py r02zb)
+  // (group term split: the slice's degrees divided again among its gsl groups)
+  __device__ __forceinline__ int kv0(int kin, int k0) const {
+    if (!TSPLIT) return kin;
+    const int a = kin + (int)((long long)(k0 - kin) * slice / S), b = kin + (int)((long long)(k0 - kin) * (slice + 1) / S);
+    return gsl > 1 && grp < gsl ? a + (b - a) * grp / gsl : a;
+  }
+  __device__ __forceinline__ int kv1(int kin, int k0) const {
+    if (TSPLIT && dead) return kv0(kin, k0);
+    if (!TSPLIT) return k0;
+    const int a = kin + (int)((long long)(k0 - kin) * slice / S), b = kin + (int)((long long)(k0 - kin) * (slice + 1) / S);
+    return gsl > 1 ? a + (b - a) * (grp + 1) / gsl : b;
+  }
+  // does this group process rank term l (of this CTA's l0 .. l1 - 1)?
+  __device__ __forceinline__ bool mine(int l) const {
+    return !TSPLIT || (!dead && (gsl == 1 || (l - l0) % gsl == grp));
   }
   __device__ __forceinline__ const double2 *vfac(long long seq, int l) const {
     if constexpr (C::STAGED) return ring.v(seq);
@@ -1022,9 +1100,9 @@ struct LineAddr {
 // whole CTA starts its batch together).  One request per 128-byte segment where the layout makes that cheap to
 // pick: the thread with vt % 16 == 0 for contiguous lines, the first of 16 consecutive lines for strided ones.
 template <class C, bool SPLIT>
-__device__ __forceinline__ void prefetch_next_line(const double *in, const Layout &lay, long long L, long long nlines,
-                                                   int vt, int n) {
-  if constexpr (JT_PREFETCH && !C::INV && C::N <= JT_PREFETCH_NMAX && C::N >= JT_PREFETCH_NMIN) {
+__device__ __forceinline__ void prefetch_line(const double *in, const Layout &lay, long long L, long long nlines, int vt,
+                                              int n) {
+  {
     if (L >= nlines) return;
     const bool mine = lay.inner == 1 ? (vt % 16 == 0) : (lay.inner % 16 == 0 ? (L % 16 == 0) : true);
     if (!mine) return;
@@ -1035,6 +1113,12 @@ __device__ __forceinline__ void prefetch_next_line(const double *in, const Layou
       if (k < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(in + ia.at(k)));
     }
   }
+}
+template <class C, bool SPLIT>
+__device__ __forceinline__ void prefetch_next_line(const double *in, const Layout &lay, long long L, long long nlines,
+                                                   int vt, int n) {
+  if constexpr (JT_PREFETCH && !C::INV && C::N <= JT_PREFETCH_NMAX && C::N >= JT_PREFETCH_NMIN)
+    prefetch_line<C, SPLIT>(in, lay, L, nlines, vt, n);
 }
 
 // Term split in clusters (TermSplit::cluster): this CTA's partial lines [line in batch][j] in its group areas.
@@ -1050,7 +1134,7 @@ __device__ __forceinline__ double *cluster_part() {
 // every CTA's partials; the second keeps each CTA's shared memory alive until its peers have read it.
 template <class C>
 __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts, const Layout &lay, long long nlines,
-                                               int n) {
+                                               int n, int r) {
   jitter();
   __syncwarp();  // (the cluster barrier is .aligned: the warp reconverges after the jitter)
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1062,19 +1146,52 @@ __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts,
   const long long E = lines * n;
   const uint32_t base = smem_u32(cluster_part<C>());
   const long long e1 = (rank + 1) * E / ts.S;
-  for (long long e = rank * E / ts.S + threadIdx.x; e < e1; e += C::NT) {
-    double sum = 0.0;
-    for (int t = 0; t < ts.S; ++t) {
-      uint32_t ra;
-      double v;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base + (uint32_t)(e * 8)), "r"(t));
-      asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
-      sum += v;
+  // (group term split, Ctx::gsl: CTA t keeps gsl_t partials of the batch's lines, group g's at g LG lines)
+  const bool gs = JT_GSPLIT > 1 && C::GPC > 1 && lines <= C::LG;
+  const uint32_t gstride = (uint32_t)(C::LG * n * 8);
+  unsigned two = 0;  // bit t: CTA t holds two partials (Ctx::gsl == 2: at least two terms)
+  if (gs)
+    for (int t = 0; t < ts.S; ++t)
+      if ((t + 1) * r / ts.S - t * r / ts.S >= 2) two |= 1u << t;
+  // two elements per thread and iteration, all 2 S remote loads in flight before the first add (one DSMEM round trip
+  // per pair instead of S per element: 256^2 forward reduction 4 -> <1 us), each summed in slice order
+  constexpr int SM_ = JT_TS_CLUSTER_MAX;
+  for (long long e = rank * E / ts.S + threadIdx.x; e < e1; e += 2 * C::NT) {
+    double v[2][SM_][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int t = 0; t < SM_; ++t) {
+        v[h][t][0] = v[h][t][1] = 0.0;
+        if (t < ts.S && e + h * C::NT < e1) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            if (g == 0 || ((two >> t) & 1u)) {
+              uint32_t ra;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                           : "=r"(ra)
+                           : "r"(base + g * gstride + (uint32_t)((e + h * C::NT) * 8)), "r"(t));
+              asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v[h][t][g]) : "r"(ra) : "memory");
+            }
+          }
+        }
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const long long eh = e + h * C::NT;
+      if (eh >= e1) break;
+      double sum = 0.0;
+#pragma unroll
+      for (int t = 0; t < SM_; ++t)
+        if (t < ts.S) {
+          sum += v[h][t][0];
+          if ((two >> t) & 1u) sum += v[h][t][1];
+        }
+      const long long lb = eh / n, j = eh - lb * n, L = L0 + lb;
+      const long long o = L / lay.inner, i = L - o * lay.inner;
+      const long long idx = (o * n + j) * lay.inner + i;
+      if (JT_CHK(idx >= 0 && idx < lay.out_lim)) out[idx] = sum;
     }
-    const long long lb = e / n, j = e - lb * n, L = L0 + lb;
-    const long long o = L / lay.inner, i = L - o * lay.inner;
-    const long long idx = (o * n + j) * lay.inner + i;
-    if (JT_CHK(idx >= 0 && idx < lay.out_lim)) out[idx] = sum;
   }
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -1087,8 +1204,16 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
                                                              long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
+  Phases phs;
+  pdl_trigger();
   Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
   cx.start(ax.bstart, ax.tw, [](int vt_, int q) { return q < R / 2 ? out_pos<C>(vt_, fwd_reg_of_bin<C>(q)) : C::N / 2; });
+  // (term split, latency-bound: the batch's input lines requested into L2 while the previous kernel finishes -- only a
+  // cache hint, so it may precede the dependency wait: L2 is the point of coherence)
+  if constexpr (TSPLIT && JT_PDL_PREFETCH)
+    prefetch_line<C, SPLIT>(in, lay, (cx.bt0 * C::GPC + cx.lgrp) * LG + cx.line, nlines, cx.vt, ax.n);
+  pdl_wait();  // (the prologue above touches only plan data: the arrays are the previous kernel's)
+  phs.mark(1);
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
   // degrees [0, kin) of W V are applied inside the term loop from the ring (KPT per term), the rest here
@@ -1100,8 +1225,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 
   long long seq = 0;
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
-    const long long L = (bt * C::GPC + cx.grp) * LG + line;
-    const bool live = L < nlines;
+    const long long L = (bt * C::GPC + cx.lgrp) * LG + line;
+    const bool live = L < nlines && (!TSPLIT || !cx.dead);
     const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
     const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs, lay.out_peer, lay.out_row);
 
@@ -1133,8 +1258,9 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int c = 0; c < MAXR; ++c) y[q][c] = 0.0;
     group_sync<C>();
+    phs.mark(2);
 #pragma unroll C::VUN
-    for (int k = kin; k < ((!TSPLIT || cx.slice == 0) ? k0 : kin); ++k) {
+    for (int k = cx.kv0(kin, k0); k < cx.kv1(kin, k0); ++k) {
       const double ak = cx.alow[k * LG + line];
       const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
 #pragma unroll
@@ -1145,9 +1271,16 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
         for (int c = 0; c < MAXR; ++c) y[q][c] = fma(pv[c], ak, y[q][c]);
       }
     }
+    phs.mark(3);
 
     for (int l = cx.l0; l < cx.l1; ++l, ++seq) {
       cx.acquire(seq);
+      if (!cx.mine(l)) {  // (another group's term, or a dead group: only the ring protocol)
+        cx.acquire_u(seq);
+        if constexpr (!C::LATE) group_sync<C>();
+        cx.release(seq);
+        continue;
+      }
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
       if constexpr (C::VST) {  // A4 for degrees l KPT .. l KPT + KPT - 1 (rows of W V staged with the term)
@@ -1300,6 +1433,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
       if constexpr (!C::LATE) group_sync<C>();  // exchange buffer and this stage are free again
       cx.release(seq);
     }
+    phs.mark(4);
 
     // (cluster term split: the partial lines go to this CTA's group areas once every group is done with them)
     double *cpart = nullptr;
@@ -1326,11 +1460,15 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
         }
       }
     }
+    phs.mark(5);
     group_sync<C>();  // alow / PRIV reuse by the next batch
   }
   cx.finish();
+  phs.mark(6);
   if constexpr (TSPLIT && C::CLUSTER_FIT)
-    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n);
+    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n, ax.r);
+  phs.mark(7);
+  phs.print(0, C::N, cx.l1 - cx.l0, lay.inner);
   if constexpr (SPLIT)
     if (lay.out_peer) __threadfence_system();  // (the fused exchange: this thread's peer stores performed system-wide)
 }
@@ -1343,8 +1481,16 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
                                                              long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
+  Phases phs;
+  pdl_trigger();
   Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
   cx.start(ax.bstart, ax.tw, [](int vt_, int q) { return q < R / 2 ? vt_ + q * TPL : C::N / 2; });
+  // (term split, latency-bound: the batch's input lines requested into L2 while the previous kernel finishes -- only a
+  // cache hint, so it may precede the dependency wait: L2 is the point of coherence)
+  if constexpr (TSPLIT && JT_PDL_PREFETCH)
+    prefetch_line<C, SPLIT>(in, lay, (cx.bt0 * C::GPC + cx.lgrp) * LG + cx.line, nlines, cx.vt, ax.n);
+  pdl_wait();  // (the prologue above touches only plan data: the arrays are the previous kernel's)
+  phs.mark(1);
   const int n = ax.n, k0 = ax.k0;
   const int vt = cx.vt, line = cx.line;
   // degrees [0, kin) of (W V)^T y are formed inside the term loop from the ring (KPT per term), the rest
@@ -1358,8 +1504,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
 
   long long seq = 0;
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
-    const long long L = (bt * C::GPC + cx.grp) * LG + line;
-    const bool live = L < nlines;
+    const long long L = (bt * C::GPC + cx.lgrp) * LG + line;
+    const bool live = L < nlines && (!TSPLIT || !cx.dead);
     const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
     const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs, lay.out_peer, lay.out_row);
 
@@ -1382,6 +1528,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
                                  : 0.0;
       }
       yb.store(yr);
+      phs.mark(2);
       prefetch_next_line<C, SPLIT>(in, lay, ((bt + cx.btstep) * C::GPC + cx.grp) * LG + line, nlines, vt, n);
       double *red = static_cast<double *>(cx.buf);  // k0 x GW x LG partials (exchange buffer is free)
       if (TSPLIT) {  // degrees outside this slice's terms contribute 0 (their slices add them)
@@ -1389,7 +1536,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         for (int i = cx.gt; i < kin * C::GW * LG; i += C::GT) cx.vred[i] = 0.0;
       }
 #pragma unroll C::VUN
-      for (int k = kin; k < ((!TSPLIT || cx.slice == 0) ? k0 : kin); ++k) {
+      for (int k = cx.kv0(kin, k0); k < cx.kv1(kin, k0); ++k) {
         const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
         double p = 0.0;
 #pragma unroll
@@ -1409,7 +1556,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       if constexpr (C::GW > 1) {
         group_sync<C>();
-        for (int i = cx.gt + kin * LG; i < ((!TSPLIT || cx.slice == 0) ? k0 : kin) * LG; i += C::GT) {
+        for (int i = cx.gt + cx.kv0(kin, k0) * LG; i < cx.kv1(kin, k0) * LG; i += C::GT) {
           const int k = i / LG, ln = i % LG;
           double s = 0.0;
 #pragma unroll
@@ -1419,6 +1566,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       }
       group_sync<C>();
     }
+    phs.mark(3);
 
     double acc[R];
 #pragma unroll
@@ -1426,6 +1574,11 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
 
     for (int l = cx.l0; l < cx.l1; ++l, ++seq) {
       cx.acquire(seq);
+      if (!cx.mine(l)) {  // (another group's term, or a dead group: only the ring protocol)
+        if constexpr (!C::LATE) group_sync<C>();
+        cx.release(seq);
+        continue;
+      }
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
       double xr[R], xi[R];
@@ -1574,6 +1727,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
       if constexpr (!C::LATE) group_sync<C>();
       cx.release(seq);
     }
+    phs.mark(4);
     if constexpr (C::VST && C::GW > 1) {  // combine the per-warp partials of degrees < kin
       if constexpr (C::LATE) group_sync<C>();  // (every warp's last partials written)
       for (int i = cx.gt; i < kin * LG; i += C::GT) {
@@ -1610,11 +1764,15 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         }
       }
     }
+    phs.mark(5);
     group_sync<C>();
   }
   cx.finish();
+  phs.mark(6);
   if constexpr (TSPLIT && C::CLUSTER_FIT)
-    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n);
+    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n, ax.r);
+  phs.mark(7);
+  phs.print(1, C::N, cx.l1 - cx.l0, lay.inner);
   if constexpr (SPLIT)
     if (lay.out_peer) __threadfence_system();  // (the fused exchange: this thread's peer stores performed system-wide)
 }
@@ -1624,7 +1782,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
 namespace jtk {
 // Sum of the S term-slice partials of a term-split launch (slice order: deterministic), written in the plain
 // (outer, n, inner) layout.  Element (o, j, i), i fastest.
-__global__ void ts_reduce(const double *__restrict__ part, double *__restrict__ out, int S, long long nlines, int n,
+static __global__ void ts_reduce(const double *__restrict__ part, double *__restrict__ out, int S, long long nlines, int n,
                           long long inner) {
   const long long total = nlines * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {

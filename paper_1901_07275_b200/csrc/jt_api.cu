@@ -17,7 +17,7 @@
 #include <thread>
 #include <vector>
 
-#include "axis_kernels.cuh"
+#include "launch.cuh"
 #include "jt_debug.h"
 #include "jt_internal.h"
 
@@ -26,18 +26,7 @@
 
 namespace {
 
-thread_local std::string g_last_error;
-
-jt_status fail(jt_status s, const std::string &msg) {
-  g_last_error = msg;
-  return s;
-}
-
-#define JT_CUDA_TRY(expr)                                                                      \
-  do {                                                                                         \
-    cudaError_t e_ = (expr);                                                                   \
-    if (e_ != cudaSuccess) return fail(JT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
+using namespace jtl;
 
 struct AxisDevBuf {
   double2 *ub = nullptr, *v = nullptr, *tw = nullptr, *tw_ts = nullptr;  // tw_ts: only if the radixes differ
@@ -59,91 +48,6 @@ struct DeviceGuard {
     if (changed) cudaSetDevice(prev);
   }
 };
-
-// SM count of the current device (cached: a driver query per launch costs microseconds on the latency-bound
-// few-line transforms).
-int sm_count() {
-  static int cache[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-  if (!cache[dev]) {
-    int v = 0;
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) return 148;
-    cache[dev] = v;
-  }
-  return cache[dev];
-}
-
-// cudaFuncSetAttribute once per (kernel, attribute, device) instead of on every launch.
-struct AttrKey {
-  const void *kern;
-  int attr, dev;
-};
-std::mutex g_attr_mu;
-std::vector<AttrKey> g_attr_done;
-cudaError_t ensure_attr(const void *kern, cudaFuncAttribute attr, int value) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  std::lock_guard<std::mutex> lk(g_attr_mu);
-  for (auto &k : g_attr_done)
-    if (k.kern == kern && k.attr == (int)attr && k.dev == dev) return cudaSuccess;
-  e = cudaFuncSetAttribute(kern, attr, value);
-  if (e == cudaSuccess) g_attr_done.push_back(AttrKey{kern, (int)attr, dev});
-  return e;
-}
-cudaError_t ensure_smem_attr(const void *kern, int smem) {
-  return ensure_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-}
-
-// Largest cluster size S <= want (down to 2) with which kernel `kern` (smem bytes per CTA) runs `need` clusters at
-// once on this device (one wave: a second wave would double the latency-bound launch); 0 if none (then the caller
-// uses the workspace + ts_reduce path).  Cached per kernel, device and request.
-struct ClusterKey {
-  const void *kern;
-  int dev, want, need, got;
-};
-std::vector<ClusterKey> g_cluster_fit;
-int cluster_fit(const void *kern, int NT, size_t smem, int want, int need) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  {
-    std::lock_guard<std::mutex> lk(g_attr_mu);
-    for (auto &k : g_cluster_fit)
-      if (k.kern == kern && k.dev == dev && k.want == want && k.need == need) return k.got;
-  }
-  int got = 0;
-  if (ensure_smem_attr(kern, (int)smem) == cudaSuccess &&
-      (want <= 8 || ensure_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
-    for (int S = want; S >= 2 && !got; --S) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)S);
-      cfg.blockDim = dim3((unsigned)NT);
-      cfg.dynamicSmemBytes = smem;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = (unsigned)S;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc >= need) got = S;
-    }
-  }
-  cudaGetLastError();  // (a refused query is not an error of the caller's)
-  std::lock_guard<std::mutex> lk(g_attr_mu);
-  g_cluster_fit.push_back(ClusterKey{kern, dev, want, need, got});
-  return got;
-}
-
-// Is stream s being captured into a CUDA graph?  (Then the calls skip their cross-call ordering events and
-// timing marks, and must not grow workspaces: capture after one uncaptured call of the same shape.)
-bool capturing(cudaStream_t s) {
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
-}
-
 }  // namespace
 
 // ---- NCCL, loaded on first use (dlopen of libnccl.so.2: the one torch already loaded, else the system's) ----
@@ -212,12 +116,9 @@ struct jt_plan_s {
   cudaEvent_t ev[2 * 16 + 2] = {};
   cudaEvent_t ev_free[JT_HOST_SLOTS] = {};  // slot's last output copy done
   unsigned host_calls = 0;
-  mutable int launches = 0;  // kernels enqueued by the latest transform call (jt_last_launches)
+  mutable jtl::LaunchState ls;  // kernels enqueued by the latest call (jt_last_launches), term-split workspace
   // slab-distributed plans (jt_plan_dist): this rank's x-slab (forward input) / y-slab
   // (forward output) of the global n[0] x n[1] (x n[2]) array, the all-to-all buffers and the NCCL comm
-  // term-split workspace (few-line launches, jtk::TermSplit); grown stream-ordered (cudaMallocAsync)
-  mutable double *ts_work = nullptr;
-  mutable size_t ts_elems = 0;
   bool dist = false;
   int rank = 0, nranks = 1;
   int dist_flags = 0;      // JT_DIST_* (jt_plan_dist_ex)
@@ -302,171 +203,6 @@ jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
   return ax;
 }
 
-// Radix of the first (register) pass for FFT length N: one SMEM exchange per term for N <= 1024
-// (16x16, 32x16, 32x32), two for 2048 and 4096 (16x16x8, 32x32x4); see DESIGN.md "Kernels".
-// MAXR = 4 (more than two nodes in some bin: only for (a, b) near the ends of (-1, 1)) always uses
-// radix 16, whose accumulators fit in registers.
-constexpr int radix_of(int64_t N, int maxr) {
-  return maxr > 2    ? 16
-         : N == 16   ? 16
-         : N == 32   ? 32
-         : N == 64   ? JT_R64
-         : N == 128  ? JT_R128
-         : N == 256  ? JT_R256
-         : N == 512  ? JT_R512
-         : N == 1024 ? JT_R1024
-         : N == 2048 ? JT_R2048
-                     : JT_R4096;
-}
-// the term-split (few-line, latency-bound) launches may use another radix (Cfg::WG instantiations)
-constexpr int radix_ts_of(int64_t N, int maxr) { return maxr <= 2 && N == 128 ? JT_R128_TS : radix_of(N, maxr); }
-template <int N, int MAXR>
-constexpr int radix_for() {
-  return radix_of(N, MAXR);
-}
-
-// The term-split instantiation of configuration C's kernel.
-template <class C>
-auto ts_kernel() {
-  if constexpr (C::INV) return jtk::inv_axis_kernel<C, false, true>;
-  else return jtk::fwd_axis_kernel<C, false, true>;
-}
-
-// Persistent launch: one CTA per SM (C::GPC groups each), looping over batches of GPC x LG lines.
-template <class C>
-jt_status launch_cfg(const jt_plan_s *p, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                     const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
-  const size_t smem = C::smem_bytes();
-  const long long lines_per_batch = (long long)C::GPC * C::LG;
-  const long long batches = (nlines + lines_per_batch - 1) / lines_per_batch;
-  if (batches == 0) return JT_OK;
-  const int sms = sm_count();
-  const bool split = lay.in_cs != ax.n || lay.out_cs != ax.n;
-  // few lines (fewer batches than half the SMs): split the rank terms over S CTAs per batch and sum the
-  // partials (jtk::TermSplit, jtk::ts_reduce), so a latency-bound launch uses more of the GPU
-  jtk::TermSplit ts{1, nullptr, 0};
-  if (allow_ts && !split && nlines == lay.outer * lay.inner && ax.r >= 2 && batches * 2 <= sms) {
-    const int S = (int)std::min<long long>(ax.r, sms / batches);
-    if constexpr (C::CLUSTER_FIT && JT_TS_CLUSTER) {
-      // the batch's S CTAs as one thread-block cluster, partials summed through distributed shared memory inside
-      // the kernel (jtk::cluster_reduce): one launch, no workspace round trip through L2 / HBM
-      auto kern = ts_kernel<C>();
-      const int Sc = S > 1 ? cluster_fit((const void *)kern, C::NT, smem, std::min(S, JT_TS_CLUSTER_MAX), (int)batches)
-                           : 0;
-      if (Sc > 1) {
-        ts = jtk::TermSplit{Sc, nullptr, 1};
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(batches * Sc));
-        cfg.blockDim = dim3((unsigned)C::NT);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)Sc;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        JT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ax, in, out, nlines, lay, ts));
-        ++p->launches;
-        return JT_OK;
-      }
-    }
-    const size_t need = (size_t)S * nlines * ax.n;
-    if (S > 1) {
-      if (p->ts_elems < need) {
-        if (capturing(s)) return fail(JT_ERR_ARG, "term-split workspace must grow: run the call once before capturing it");
-        // stream-ordered: no implicit device synchronisation in the middle of a pipelined call (a ragged later
-        // chunk may need more than an earlier one), and valid under CUDA graph capture
-        if (p->ts_work) cudaFreeAsync(p->ts_work, s);
-        p->ts_work = nullptr;
-        p->ts_elems = 0;
-        if (cudaMallocAsync((void **)&p->ts_work, need * sizeof(double), s) != cudaSuccess)
-          return fail(JT_ERR_ALLOC, "term-split workspace");
-        p->ts_elems = need;
-      }
-      ts = jtk::TermSplit{S, p->ts_work, 0};
-    }
-  }
-  const unsigned grid = ts.S > 1 ? (unsigned)(batches * ts.S) : (unsigned)std::min<long long>(batches, sms);
-  if constexpr (C::WG && !JT_WG_LARGE) {  // (only reached for term-split launches: see launch_nmd)
-    if (ts.S <= 1) return fail(JT_ERR_ARG, "internal: one-warp-group configuration without term split");
-    if constexpr (C::INV) {
-      JT_CUDA_TRY(ensure_smem_attr((const void *)jtk::inv_axis_kernel<C, false, true>, (int)smem));
-      jtk::inv_axis_kernel<C, false, true><<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
-    } else {
-      JT_CUDA_TRY(ensure_smem_attr((const void *)jtk::fwd_axis_kernel<C, false, true>, (int)smem));
-      jtk::fwd_axis_kernel<C, false, true><<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
-    }
-  } else if constexpr (C::INV) {
-    auto kern = ts.S > 1 ? jtk::inv_axis_kernel<C, false, true>
-                         : (split ? jtk::inv_axis_kernel<C, true> : jtk::inv_axis_kernel<C, false>);
-    JT_CUDA_TRY(ensure_smem_attr((const void *)kern, (int)smem));
-    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
-  } else {
-    auto kern = ts.S > 1 ? jtk::fwd_axis_kernel<C, false, true>
-                         : (split ? jtk::fwd_axis_kernel<C, true> : jtk::fwd_axis_kernel<C, false>);
-    JT_CUDA_TRY(ensure_smem_attr((const void *)kern, (int)smem));
-    kern<<<grid, C::NT, smem, s>>>(ax, in, out, nlines, lay, ts);
-  }
-  JT_CUDA_TRY(cudaGetLastError());
-  ++p->launches;
-  if (ts.S > 1) {
-    ++p->launches;
-    const long long total = nlines * ax.n;
-    const int thr = 256;
-    const unsigned g = (unsigned)std::min<long long>((total + thr - 1) / thr, 4LL * sms);
-    jtk::ts_reduce<<<g, thr, 0, s>>>(ts.part, out, ts.S, nlines, ax.n, lay.inner);
-    JT_CUDA_TRY(cudaGetLastError());
-  }
-  return JT_OK;
-}
-
-// Would launch_cfg<C> split the rank terms (few lines)?  Same test as inside launch_cfg.
-template <class C>
-bool term_split_applies(const jtk::AxisDev &ax, long long nlines, const jtk::Layout &lay, bool allow_ts, int sms) {
-  const long long batches = (nlines + (long long)C::GPC * C::LG - 1) / ((long long)C::GPC * C::LG);
-  const bool split = lay.in_cs != ax.n || lay.out_cs != ax.n;
-  return allow_ts && !split && nlines == lay.outer * lay.inner && ax.r >= 2 && batches > 0 && batches * 2 <= sms &&
-         std::min<long long>(ax.r, sms / batches) > 1;
-}
-
-template <int N, int MAXR, bool INV>
-jt_status launch_nmd(const jt_plan_s *p, const jtk::AxisDev &ax, const double *in, double *out, long long nlines,
-                     const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
-  using C = jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, INV>;
-  using CW = jtk::Cfg<N, radix_ts_of(N, MAXR), MAXR, INV, true>;
-  if constexpr (CW::LG != C::LG || CW::R != C::R) {  // term-split launches: one-warp groups / their own radix
-    const int sms = sm_count();
-    if (term_split_applies<CW>(ax, nlines, lay, allow_ts, sms)) {
-      jtk::AxisDev axt = ax;
-      axt.tw = ax.tw_ts;
-      return launch_cfg<CW>(p, axt, in, out, nlines, lay, s, true);
-    }
-    if constexpr (JT_WG_LARGE && N == JT_WG_LARGE && CW::R == C::R) {  // (A/B: one-warp groups for every launch)
-      jtk::AxisDev axt = ax;
-      axt.tw = ax.tw_ts;
-      return launch_cfg<CW>(p, axt, in, out, nlines, lay, s, allow_ts);
-    }
-  }
-  return launch_cfg<C>(p, ax, in, out, nlines, lay, s, allow_ts);
-}
-
-template <int N, int MAXR>
-jt_status launch_nm(const jt_plan_s *p, bool inverse, const jtk::AxisDev &ax, const double *in, double *out,
-                    long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
-  if (inverse) return launch_nmd<N, MAXR, true>(p, ax, in, out, nlines, lay, s, allow_ts);
-  return launch_nmd<N, MAXR, false>(p, ax, in, out, nlines, lay, s, allow_ts);
-}
-
-template <int N>
-jt_status launch_n(const jt_plan_s *p, bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out,
-                   long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
-  if (maxr <= 2) return launch_nm<N, 2>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
-  if (maxr == 3) return launch_nm<N, 3>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
-  return launch_nm<N, 4>(p, inverse, ax, in, out, nlines, lay, s, allow_ts);
-}
-
 // One axis pass over the (outer, n[axis], inner) array; in_split / out_split = G > 1 selects the chunk-major
 // layout of the slab all-to-all for the input / output.
 // in_lim / out_lim: elements of the input / output buffers from the given pointers (bounds of the JT_CHECKS
@@ -492,15 +228,15 @@ jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *
                         in_lim >= 0 ? in_lim : geo_in, out_lim >= 0 ? out_lim : geo_out,
                         peer ? p->d_peer_off : nullptr, peer ? peer_row : 0};
   switch (ax.N) {
-    case 16: return launch_n<16>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 32: return launch_n<32>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 64: return launch_n<64>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 128: return launch_n<128>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 256: return launch_n<256>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 512: return launch_n<512>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 1024: return launch_n<1024>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 2048: return launch_n<2048>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
-    case 4096: return launch_n<4096>(p, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 16: return launch_n<16>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 32: return launch_n<32>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 64: return launch_n<64>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 128: return launch_n<128>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 256: return launch_n<256>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 512: return launch_n<512>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 1024: return launch_n<1024>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 2048: return launch_n<2048>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
+    case 4096: return launch_n<4096>(p->ls, inverse, maxr, ax, in, out, nlines, lay, s, allow_ts);
     default: return fail(JT_ERR_ARG, "unsupported FFT length");
   }
 }
@@ -537,9 +273,9 @@ void free_device(jt_plan_s *p) {
     p->stage_in[k] = p->stage_out[k] = nullptr;
     if (p->ev_free[k]) cudaEventDestroy(p->ev_free[k]), p->ev_free[k] = nullptr;
   }
-  cudaFree(p->ts_work);
-  p->ts_work = nullptr;
-  p->ts_elems = 0;
+  cudaFree(p->ls.ts_work);
+  p->ls.ts_work = nullptr;
+  p->ls.ts_elems = 0;
   for (int g = 0; g < jtk::MAX_SPLIT; ++g)
     if (p->peer_ipc[g]) cudaIpcCloseMemHandle(p->peer_recv[g]), p->peer_ipc[g] = false;
   cudaFree(p->bar_buf);
@@ -962,7 +698,7 @@ jt_status transform_body(const jt_plan_s *p, bool inverse, const double *in, dou
 
 jt_status transform(const jt_plan_s *p, bool inverse, const double *in, double *out, cudaStream_t s) {
   jt_status st = check_device_plan(p);
-  p->launches = 0;
+  p->ls.launches = 0;
   if (st != JT_OK) return st;
   if (!in || !out) return fail(JT_ERR_ARG, "null data pointer");
   if (overlaps_partially(in, out, p->total)) return fail(JT_ERR_ARG, "input and output partially overlap");
@@ -1010,7 +746,7 @@ jt_status host_wait(jt_plan_s *p) {
 jt_status transform_host(jt_plan_s *p, bool inverse, const double *in_h, double *out_h, cudaStream_t s,
                          bool wait) {
   jt_status st = check_device_plan(p);
-  p->launches = 0;
+  p->ls.launches = 0;
   if (st != JT_OK) return st;
   if (!in_h || !out_h) return fail(JT_ERR_ARG, "null host pointer");
   DeviceGuard g(p->device);
@@ -1236,7 +972,7 @@ const char *jt_version(void) { return "jt 0.1 (sm_100a fused fp64 axis passes)";
 
 jt_status jt_last_launches(jt_plan_t p, int *count) {
   if (!p || !count) return fail(JT_ERR_ARG, "null argument");
-  *count = p->launches;
+  *count = p->ls.launches;
   return JT_OK;
 }
 
@@ -1405,7 +1141,7 @@ jt_status jt_inverse_host(jt_plan_t p, const double *values_host, double *coeffs
 static jt_status axis_entry(jt_plan_t p, int axis, bool inverse, const double *in, double *out, int64_t outer,
                             int64_t inner, int in_split, int out_split, void *stream, int64_t ostride = -1) {
   jt_status st = check_device_plan(p);
-  if (p) p->launches = 0;
+  if (p) p->ls.launches = 0;
   if (st != JT_OK) return st;
   if (axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad axis");
   if (!in || !out || outer < 0 || inner < 1) return fail(JT_ERR_ARG, "bad pointers / shape");
@@ -1640,7 +1376,7 @@ jt_status jt_debug_axis_pass_lim(jt_plan_t p, int axis, int inverse, const doubl
   if (st != JT_OK) return st;
   if (axis < 0 || axis >= p->d || !in || !out || outer < 1 || inner < 1 || in_lim < 0 || out_lim < 0)
     return fail(JT_ERR_ARG, "bad args");
-  p->launches = 0;
+  p->ls.launches = 0;
   DeviceGuard g(p->device);
   const cudaStream_t s = (cudaStream_t)stream;
   if ((st = begin_call(p, s)) != JT_OK) return st;
@@ -1656,14 +1392,13 @@ jt_status jt_debug_checks(int *enabled, unsigned long long *count, int *line) {
   unsigned long long c = 0;
   int l = 0;
   JT_CUDA_TRY(cudaDeviceSynchronize());
-  JT_CUDA_TRY(cudaMemcpyFromSymbol(&c, jtk::jt_check_count, sizeof(c)));
-  JT_CUDA_TRY(cudaMemcpyFromSymbol(&l, jtk::jt_check_line, sizeof(l)));
+  jt_status st = JT_OK;
+  for (jt_status (*io)(unsigned long long *, int *) :
+       {checks_io<16>, checks_io<32>, checks_io<64>, checks_io<128>, checks_io<256>, checks_io<512>, checks_io<1024>,
+        checks_io<2048>, checks_io<4096>})
+    if ((st = io(&c, &l)) != JT_OK) return st;
   *count = c;
   *line = l;
-  const unsigned long long z = 0;
-  const int zl = 0;
-  JT_CUDA_TRY(cudaMemcpyToSymbol(jtk::jt_check_count, &z, sizeof(z)));
-  JT_CUDA_TRY(cudaMemcpyToSymbol(jtk::jt_check_line, &zl, sizeof(zl)));
   return JT_OK;
 }
 

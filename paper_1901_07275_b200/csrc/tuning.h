@@ -138,6 +138,16 @@
 #define JT_WG_LARGE 0  // N: the one-warp-group configuration (Cfg::WG) for every launch of FFT length N, not only
                        // the term-split ones (0: off)
 #endif
+#ifndef JT_GSPLIT
+#define JT_GSPLIT 2  // group term split (2 or 0 = off): up to this many groups of a term-split CTA share its terms when the batch fits
+                     // in one group (1D transforms; 0: off; the cluster reduction reads at most 2 partials per CTA)
+#endif
+#ifndef JT_PDL
+#define JT_PDL 1  // axis-pass kernels launched with programmatic dependent launch (prologue overlaps the previous tail)
+#endif
+#ifndef JT_PDL_PREFETCH
+#define JT_PDL_PREFETCH 1  // term-split launches: L2 prefetch of the batch's input lines before the dependency wait
+#endif
 #ifndef JT_HOST_SCHED
 #define JT_HOST_SCHED 2  // single-GPU *_host pipeline: 0 = axes d-1..1 on arriving row chunks, then axis 0 in column
                          // blocks copied back pitched; 1 = axis 0 first, then row chunks copied back contiguous;
