@@ -9,6 +9,7 @@ import os
 import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -57,10 +58,12 @@ def build(verbose_ptxas: bool = False, out: str = LIB, defines=(), tag: str = ""
     only for the default build) also libjt_checks.so.  All translation units compile in parallel."""
     nvcc = _nvcc()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
-    build_dir = os.path.join(HERE, "_build")
+    # object files outside the repository (they need not travel to the GPU box with the libraries)
+    build_dir = os.environ.get("JT_BUILD_DIR") or os.path.join(tempfile.gettempdir(), "jt_build")
     os.makedirs(build_dir, exist_ok=True)
     plan_o = os.path.join(build_dir, "plan.o")
-    base = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", *inc]
+    # (compressed fatbins: one translation unit per FFT length repeats the line tables, 45 -> ~15 MB per library)
+    base = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xfatbin=-compress-all", *inc]
     if verbose_ptxas:
         base += ["-Xptxas", "-v"]
     variants = [(out, tag, [f"-D{d}" for d in defines])]

@@ -70,7 +70,33 @@ struct TermSplit {
   // partial lines are summed through distributed shared memory at the end of the kernel (cluster_reduce): no
   // workspace, no ts_reduce launch
   int cluster;
+  // in_S > 0 (term-split launches only): the input is the sum, in slice order, of in_S arrays at in_part + s in_stride
+  // (the previous pass's partials, not reduced by a launch of their own: the reduction fused into this pass's loads)
+  const double *in_part = nullptr;
+  long long in_stride = 0;
+  int in_S = 0;
 };
+
+// Input element at offset idx: the plain input, or (fused reduction) the sum of the previous pass's partials.
+// (compiled only with JT_TS_FUSE: the runtime branch alone cost the 1D forward 3 us -- the plain input loads no longer
+// all issue before the first use)
+template <bool TSPLIT>
+__device__ __forceinline__ double load_in(const double *in, const TermSplit &ts, long long idx) {
+  if constexpr (TSPLIT && JT_TS_FUSE) {
+    if (ts.in_S > 0) {
+      double v[4], sum = 0.0;
+      for (int s0 = 0; s0 < ts.in_S; s0 += 4) {  // four partials' loads in flight per round
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = s0 + q < ts.in_S ? __ldg(&ts.in_part[(s0 + q) * ts.in_stride + idx]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (s0 + q < ts.in_S) sum += v[q];
+      }
+      return sum;
+    }
+  }
+  return __ldg(&in[idx]);
+}
 
 // (build-time tuning knobs JT_*: tuning.h)
 
@@ -118,7 +144,7 @@ __device__ __forceinline__ void jitter() {
 #endif
 struct Phases {
 #if JT_PHASES
-  long long t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long g0 = 0;
   __device__ __forceinline__ Phases() {
     if (threadIdx.x == 0) {
@@ -136,9 +162,10 @@ struct Phases {
       const long long e = clock64();
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      printf("PH k%d_i%lld n%d cta%d sm%u terms%d g0 %llu g1 %llu d %lld %lld %lld %lld %lld %lld %lld %lld\n", kind, inner,
-             n, (int)blockIdx.x, smid, terms, g0, g1, t[1] - t[0], t[2] - t[0], t[3] - t[0], t[4] - t[0], t[5] - t[0],
-             t[6] - t[0], t[7] - t[0], e - t[0]);
+      printf("PH k%d_i%lld n%d cta%d sm%u terms%d g0 %llu g1 %llu d %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
+             kind, inner, n, (int)blockIdx.x, smid, terms, g0, g1, t[1] - t[0], t[2] - t[0], t[3] - t[0], t[4] - t[0],
+             t[5] - t[0], t[6] - t[0], t[8] ? t[8] - t[0] : 0, t[9] ? t[9] - t[0] : 0, t[10] ? t[10] - t[0] : 0,
+             t[7] - t[0], e - t[0]);
     }
   }
 #else
@@ -309,7 +336,11 @@ struct Cfg {
                ? gpc_fit(g - 1, nstage)
                : g;
   }
-  static constexpr int GPC = gpc_fit(8, STAGED ? 2 : (SUB ? 4 : 1));  // groups per CTA (one CTA per SM)
+  // groups per CTA (one CTA per SM; the one-warp-group term-split configurations can cap it at JT_WG_GPC so that
+  // two CTAs share an SM: twice the CTAs, each with fewer rank terms)
+  static constexpr int GPC = (WG && JT_WG_GPC < gpc_fit(8, STAGED ? 2 : (SUB ? 4 : 1))) ? JT_WG_GPC
+                                                                                   : gpc_fit(8, STAGED ? 2 : (SUB ? 4 : 1));
+  static constexpr int MINB = WG && JT_WG_GPC < 8 ? 2 : 1;  // __launch_bounds__ min blocks
   // LATE: no group barrier at the end of a rank term; the exchange buffer's reuse is guarded by a barrier just
   // before the next term's first exchange store (and a ring stage, where there is one, is released per warp), so a
   // warp can run into the next term's column scale and first DFT pass ahead of its group's other warps.  Measured
@@ -776,13 +807,15 @@ __device__ __forceinline__ void run_passes(double (&xr)[C::R], double (&xi)[C::R
 
 // Full FFT of one term; first-pass inputs (positions vt + r TPL) in registers on entry, last-pass
 // outputs (positions out_pos) in registers on exit.  The caller syncs the group before the next call.
-template <class C, bool PRE = false>
+// Z: the first-pass inputs above position R/2 of the thread are zero (the inverse: bins > N/2 hold no rows)
+template <class C, bool PRE = false, bool Z = false>
 __device__ __forceinline__ void fft(double (&xr)[C::R], double (&xi)[C::R], void *buf, int vt, int line,
                                     const double2 *__restrict__ tw, uint32_t ttw) {
   using P0 = Pass<C::N, C::R, 1>;
   static_assert(!PRE || (P0::RS == 32 && P0::B == 1), "PRE: one radix-32 first pass");
+  constexpr bool ZZ = Z && JT_ZFIRST && P0::B == 1 && (P0::RS == 16 || P0::RS == 32);
 #pragma unroll
-  for (int i = 0; i < P0::B; ++i) dft<P0::RS, PRE>(&xr[i * P0::RS], &xi[i * P0::RS]);
+  for (int i = 0; i < P0::B; ++i) dft<P0::RS, PRE, ZZ>(&xr[i * P0::RS], &xi[i * P0::RS]);
   if constexpr (!P0::LAST) {
     if constexpr (C::LATE) group_sync<C>();  // every thread of the group has read the previous term's exchange
     do_exchange<C, 1>(xr, xi, buf, vt, line);
@@ -1134,10 +1167,11 @@ __device__ __forceinline__ double *cluster_part() {
 // every CTA's partials; the second keeps each CTA's shared memory alive until its peers have read it.
 template <class C>
 __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts, const Layout &lay, long long nlines,
-                                               int n, int r) {
+                                               int n, int r, Phases &phs) {
   jitter();
   __syncwarp();  // (the cluster barrier is .aligned: the warp reconverges after the jitter)
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  phs.mark(8);
   unsigned rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const long long bt = blockIdx.x / ts.S;
@@ -1156,14 +1190,20 @@ __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts,
   // two elements per thread and iteration, all 2 S remote loads in flight before the first add (one DSMEM round trip
   // per pair instead of S per element: 256^2 forward reduction 4 -> <1 us), each summed in slice order
   constexpr int SM_ = JT_TS_CLUSTER_MAX;
-  for (long long e = rank * E / ts.S + threadIdx.x; e < e1; e += 2 * C::NT) {
+  // element e = lb n + j of the batch: (lb, j) advanced incrementally (no 64-bit division per element), the output
+  // offset recomputed only when the line changes
+  const int e0 = (int)(rank * E / ts.S) + (int)threadIdx.x;
+  int lb = e0 / n, j = e0 - lb * n;
+  long long obase = -1;
+  int olb = -1;
+  for (int e = e0; e < (int)e1; e += 2 * C::NT) {
     double v[2][SM_][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int t = 0; t < SM_; ++t) {
         v[h][t][0] = v[h][t][1] = 0.0;
-        if (t < ts.S && e + h * C::NT < e1) {
+        if (t < ts.S && e + h * C::NT < (int)e1) {
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             if (g == 0 || ((two >> t) & 1u)) {
@@ -1178,8 +1218,7 @@ __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts,
       }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const long long eh = e + h * C::NT;
-      if (eh >= e1) break;
+      if (e + h * C::NT >= (int)e1) break;
       double sum = 0.0;
 #pragma unroll
       for (int t = 0; t < SM_; ++t)
@@ -1187,20 +1226,134 @@ __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts,
           sum += v[h][t][0];
           if ((two >> t) & 1u) sum += v[h][t][1];
         }
-      const long long lb = eh / n, j = eh - lb * n, L = L0 + lb;
-      const long long o = L / lay.inner, i = L - o * lay.inner;
-      const long long idx = (o * n + j) * lay.inner + i;
+      if (lb != olb) {
+        const long long L = L0 + lb, o = L / lay.inner, i = L - o * lay.inner;
+        obase = o * n * lay.inner + i;
+        olb = lb;
+      }
+      const long long idx = obase + (long long)j * lay.inner;
       if (JT_CHK(idx >= 0 && idx < lay.out_lim)) out[idx] = sum;
+      j += C::NT;
+      while (j >= n) {
+        j -= n;
+        ++lb;
+      }
     }
   }
+  phs.mark(9);
+  // (only keeps every CTA's shared memory alive until its peers' loads returned -- they have: their values were summed
+  // -- so a relaxed arrive: the release form's GPU-scope fence waited ~1-2 us for the output stores to drain)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+  phs.mark(10);
+}
+
+// Push form of the cluster reduction (JT_TS_PUSH): instead of every CTA pulling its element range from the S peers
+// with 8-byte remote loads (measured ~3.5 us for 8-32 KB per CTA: many small requests over the SM-to-SM network),
+// every CTA sends each owner t its partials of t's range with ONE bulk copy (cp.async.bulk shared::cta ->
+// shared::cluster, completion on t's mbarrier), into a receive area in t's factor-ring region (free after the term
+// loop); the owner sums its S (or S + the CTAs' second-group) slots locally, in slice order -- the order of the pull
+// form and of ts_reduce, so results are bit-identical.  Ranges start at even elements (16-byte aligned copies).
+// Returns false (nothing done) where the receive area does not fit: the caller then uses cluster_reduce.
+template <class C>
+__device__ __forceinline__ bool cluster_reduce_push(double *out, const TermSplit &ts, const Layout &lay,
+                                                    long long nlines, int n, int r, Phases &phs) {
+  extern __shared__ __align__(128) char smem_raw[];
+  const int S = ts.S;
+  const long long bt = blockIdx.x / S;
+  const long long L0 = bt * C::GPC * C::LG;
+  const int lines = (int)min((long long)C::GPC * C::LG, nlines - L0);
+  const int E = lines * n;
+  const bool gs = JT_GSPLIT > 1 && C::GPC > 1 && lines <= C::LG;
+  unsigned two = 0;
+  if (gs)
+    for (int t = 0; t < S; ++t)
+      if ((t + 1) * r / S - t * r / S >= 2) two |= 1u << t;
+  const int slots = gs ? 2 * S : S;
+  const int RS = ((E + S - 1) / S + 3) & ~1;  // receive slot stride (doubles, even) >= every range + 1
+  const int recv_bytes = slots * RS * 8;
+  // (uniform over the cluster: every CTA takes the same branch)
+  if (recv_bytes + 16 > C::HDR_BYTES || (gs && (C::LG * n) % 2 != 0)) return false;
+  double *recv = reinterpret_cast<double *>(smem_raw);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem_raw + ((recv_bytes + 15) & ~15));
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  auto ra = [&](int t) { return t <= 0 ? 0 : (t >= S ? E : ((int)((long long)t * E / S) & ~1)); };
+  const int a = ra((int)rank), b = ra((int)rank + 1);
+  const uint32_t my_bytes = (uint32_t)(((b - a) * 8 + 15) & ~15);
+  if (threadIdx.x == 0) {
+    // (the ring's stage barriers live in this region: invalidated before it is reused as data)
+    if constexpr (C::STAGED || C::URING || C::SUB)
+      for (int st = 0; st < C::NSTAGE; ++st)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(reinterpret_cast<uint64_t *>(
+                         smem_raw + C::NSTAGE * C::STAGE_BYTES) + st))
+                     : "memory");
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive_expect_tx(mbar, my_bytes * (uint32_t)(S + __popc(two)));
+  }
+  jitter();
+  __syncwarp();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  phs.mark(8);
+  if ((int)threadIdx.x < S) {  // thread t: this CTA's partials of owner t's range, one bulk copy per group partial
+    const int t = threadIdx.x, at = ra(t), btt = ra(t + 1);
+    const uint32_t bytes = (uint32_t)(((btt - at) * 8 + 15) & ~15);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (the partials were written by generic stores)
+    const uint32_t src = smem_u32(cluster_part<C>() + at);
+    uint32_t dst, mb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(recv + rank * RS)), "r"(t));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(mb) : "r"(smem_u32(mbar)), "r"(t));
+    if (bytes)
+      asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                   "r"(src), "r"(bytes), "r"(mb)
+                   : "memory");
+    if ((two >> rank) & 1u) {  // the second group's partial (Ctx::gsl == 2) into slot S + rank
+      const uint32_t src2 = smem_u32(cluster_part<C>() + C::LG * n + at);
+      uint32_t dst2;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst2) : "r"(smem_u32(recv + (S + rank) * RS)), "r"(t));
+      if (bytes)
+        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dst2),
+                     "r"(src2), "r"(bytes), "r"(mb)
+                     : "memory");
+    }
+  }
+  mbar_wait(mbar, 0);
+  __syncwarp();
+  phs.mark(9);
+  // owner: elements [a, b) of the batch, summed over the slots in slice order (second-group partial after each slice)
+  int lb = (a + (int)threadIdx.x) / n, j = a + (int)threadIdx.x - lb * n, olb = -1;
+  long long obase = 0;
+  for (int k = threadIdx.x; k < b - a; k += C::NT) {
+    double sum = 0.0;
+    for (int t = 0; t < S; ++t) {
+      sum += recv[t * RS + k];
+      if ((two >> t) & 1u) sum += recv[(S + t) * RS + k];
+    }
+    if (lb != olb) {
+      const long long L = L0 + lb, o = L / lay.inner, i = L - o * lay.inner;
+      obase = o * n * lay.inner + i;
+      olb = lb;
+    }
+    const long long idx = obase + (long long)j * lay.inner;
+    if (JT_CHK(idx >= 0 && idx < lay.out_lim)) out[idx] = sum;
+    j += C::NT;
+    while (j >= n) {
+      j -= n;
+      ++lb;
+    }
+  }
+  // every copy out of this CTA's shared memory has completed (its owner waited for it) before anyone exits
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+  phs.mark(10);
+  return true;
 }
 
 // ------------------------------------------------------------------------------------------------
 // Forward axis pass (K4).
 // ------------------------------------------------------------------------------------------------
 template <class C, bool SPLIT, bool TSPLIT = false>
-__global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
+__global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, const double *in, double *out,
                                                              long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
@@ -1238,7 +1391,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int k = vt + r * TPL;
-        av[r] = (live && k < n && JT_CHK(ia.at(k) >= 0 && ia.at(k) < lay.in_lim)) ? __ldg(&in[ia.at(k)]) : 0.0;
+        av[r] = (live && k < n && JT_CHK(ia.at(k) >= 0 && ia.at(k) < lay.in_lim)) ? load_in<TSPLIT>(in, ts, ia.at(k)) : 0.0;
       }
       a.store(av);
 #pragma unroll
@@ -1466,7 +1619,8 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
   cx.finish();
   phs.mark(6);
   if constexpr (TSPLIT && C::CLUSTER_FIT)
-    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n, ax.r);
+    if (ts.cluster && !(JT_TS_PUSH && cluster_reduce_push<C>(out, ts, lay, nlines, n, ax.r, phs)))
+      cluster_reduce<C>(out, ts, lay, nlines, n, ax.r, phs);
   phs.mark(7);
   phs.print(0, C::N, cx.l1 - cx.l0, lay.inner);
   if constexpr (SPLIT)
@@ -1477,7 +1631,7 @@ __global__ void __launch_bounds__(C::NT, 1) fwd_axis_kernel(AxisDev ax, const do
 // Inverse axis pass (K5).
 // ------------------------------------------------------------------------------------------------
 template <class C, bool SPLIT, bool TSPLIT = false>
-__global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const double *in, double *out,
+__global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, const double *in, double *out,
                                                              long long nlines, Layout lay, TermSplit ts) {
   constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
   extern __shared__ __align__(128) char smem_raw[];
@@ -1524,7 +1678,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
         for (int c = 0; c < MAXR; ++c)
           yr[q * MAXR + c] = (live && own && c < cnt && JT_CHK(j0 + c < n && m[q] < NBINS) &&
                               JT_CHK(ia.at(j0 + c) >= 0 && ia.at(j0 + c) < lay.in_lim))
-                                 ? __ldg(&in[ia.at(j0 + c)])
+                                 ? load_in<TSPLIT>(in, ts, ia.at(j0 + c))
                                  : 0.0;
       }
       yb.store(yr);
@@ -1696,7 +1850,7 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
 #pragma unroll
         for (int e = 0; e < R; ++e) asm volatile("prefetch.global.L1 [%0];" ::"l"(vl + out_pos<C>(vt, e)));
       }
-      fft<C>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);
+      fft<C, false, true>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // (inputs above R/2: empty bins)
       if constexpr (C::SUB) {
         // a[k] += Re(v_l[k] B[k]) from the ring: sub-stage 4 + j holds v_l[1024 h + 256 j + ...], i.e. the outputs
         // e with e / RSL in {2j, 2j + 1} (k = vt + (e / RSL) TPL + (e % RSL) N / RSL, RSL = 4)
@@ -1770,7 +1924,8 @@ __global__ void __launch_bounds__(C::NT, 1) inv_axis_kernel(AxisDev ax, const do
   cx.finish();
   phs.mark(6);
   if constexpr (TSPLIT && C::CLUSTER_FIT)
-    if (ts.cluster) cluster_reduce<C>(out, ts, lay, nlines, n, ax.r);
+    if (ts.cluster && !(JT_TS_PUSH && cluster_reduce_push<C>(out, ts, lay, nlines, n, ax.r, phs)))
+      cluster_reduce<C>(out, ts, lay, nlines, n, ax.r, phs);
   phs.mark(7);
   phs.print(1, C::N, cx.l1 - cx.l0, lay.inner);
   if constexpr (SPLIT)

@@ -75,14 +75,34 @@ JT_DEV void dft4_pre(double *xr, double *xi) {
   xr[3] = t1r + t3i; xi[3] = t1i - t3r;
 }
 
-template <int M, bool PRE = false>
+// dft4 with x[3] = 0, and with x[2] = x[3] = 0 (Z: the inverse's first pass, whose inputs above M/2 are empty bins)
+JT_DEV void dft4_z1(double *xr, double *xi) {
+  const double t0r = xr[0] + xr[2], t0i = xi[0] + xi[2];
+  const double t1r = xr[0] - xr[2], t1i = xi[0] - xi[2];
+  const double br = xr[1], bi = xi[1];
+  xr[0] = t0r + br; xi[0] = t0i + bi;
+  xr[2] = t0r - br; xi[2] = t0i - bi;
+  xr[1] = t1r - bi; xi[1] = t1i + br;
+  xr[3] = t1r + bi; xi[3] = t1i - br;
+}
+JT_DEV void dft4_z2(double *xr, double *xi) {
+  const double ar = xr[0], ai = xi[0], br = xr[1], bi = xi[1];
+  xr[0] = ar + br; xi[0] = ai + bi;
+  xr[2] = ar - br; xi[2] = ai - bi;
+  xr[1] = ar - bi; xi[1] = ai + br;
+  xr[3] = ar + bi; xi[3] = ai - br;
+}
+
+template <int M, bool PRE = false, bool Z = false>
 JT_DEV void dft(double *xr, double *xi);
 
 // Cooley-Tukey M = N1 N2 in registers: n = N2 n1 + n2, k = k1 + N1 k2.
 //   Y[k1][n2] = DFT_N1 over n1 of x[N2 n1 + n2];  Y *= w_M^{n2 k1};  X[k1 + N1 k2] = DFT_N2 over n2.
 // PRE (N1 = 4): the inputs already hold the first butterfly layer of the DFT_4s, x[n] +- x[n + M/2] at n and
 // n + M/2 (n < M/2) -- the forward's column scale computes them with FMAs (dft<32, true>).
-template <int N1, int N2, bool PRE = false>
+// Z (N1 = 4): inputs x[n] = 0 for n > M/2 (skipped: the first layer of the DFT_4s of n2 >= 1 has two zero inputs, that
+// of n2 = 0 one), 60 of ~1100 FP64 instructions per thread and term in the radix-32 inverse.
+template <int N1, int N2, bool PRE = false, bool Z = false>
 JT_DEV void dft_ct(double *xr, double *xi) {
   constexpr int M = N1 * N2;
   double yr[M], yi[M];
@@ -94,6 +114,10 @@ JT_DEV void dft_ct(double *xr, double *xi) {
     if constexpr (PRE) {
       static_assert(N1 == 4, "PRE: first layer of DFT_4");
       dft4_pre(ar, ai);
+    } else if constexpr (Z) {
+      static_assert(N1 == 4, "Z: first layer of DFT_4");
+      if (n2 == 0) dft4_z1(ar, ai);
+      else dft4_z2(ar, ai);
     } else {
       dft<N1>(ar, ai);
     }
@@ -115,9 +139,10 @@ JT_DEV void dft_ct(double *xr, double *xi) {
   }
 }
 
-template <int M, bool PRE>
+template <int M, bool PRE, bool Z>
 JT_DEV void dft(double *xr, double *xi) {
   static_assert(!PRE || M == 32, "PRE: radix 32 only");
+  static_assert(!Z || M == 16 || M == 32, "Z: radix 16 / 32 only");
   if constexpr (M == 1) {
   } else if constexpr (M == 2) {
     dft2(xr, xi);
@@ -126,9 +151,9 @@ JT_DEV void dft(double *xr, double *xi) {
   } else if constexpr (M == 8) {
     dft_ct<2, 4>(xr, xi);
   } else if constexpr (M == 16) {
-    dft_ct<4, 4>(xr, xi);
+    dft_ct<4, 4, false, Z>(xr, xi);
   } else if constexpr (M == 32) {
-    dft_ct<4, 8, PRE>(xr, xi);
+    dft_ct<4, 8, PRE, Z>(xr, xi);
   } else {
     static_assert(M <= 32, "radix too large");
   }

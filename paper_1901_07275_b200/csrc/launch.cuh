@@ -21,6 +21,15 @@ struct LaunchState {
   int launches = 0;
   double *ts_work = nullptr;
   size_t ts_elems = 0;
+  // fused term-split reduction (jt_api.cu transform_body): mode 1 = only report what the launch would do (q_S term
+  // slices, q_cluster: reduced in a cluster), mode 2 = a workspace term split that leaves its q_S partials in ts_work
+  // (no ts_reduce); in_S > 0: the next launch's input is the sum of those partials (TermSplit::in_part)
+  int mode = 0;
+  int q_S = 1;
+  bool q_cluster = false;
+  const double *in_part = nullptr;
+  long long in_stride = 0;
+  int in_S = 0;
 };
 
 inline thread_local std::string g_last_error;
@@ -115,6 +124,30 @@ inline int cluster_fit(const void *kern, int NT, size_t smem, int want, int need
   return got;
 }
 
+// Resident CTAs per SM of kernel `kern` (NT threads, smem bytes), at most 2 and at least 1 (cached).
+struct OccKey {
+  const void *kern;
+  int dev, nt;
+  size_t smem;
+  int got;
+};
+inline std::vector<OccKey> g_occ;
+inline int blocks_per_sm(const void *kern, int NT, size_t smem) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (auto &k : g_occ)
+    if (k.kern == kern && k.dev == dev && k.nt == NT && k.smem == smem) return k.got;
+  int nb = 1;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, smem) != cudaSuccess || nb < 1)
+    nb = 1;
+  cudaGetLastError();
+  nb = std::min(nb, 2);
+  g_occ.push_back(OccKey{kern, dev, NT, smem, nb});
+  return nb;
+}
+
 // Is stream s being captured into a CUDA graph?  (Then the calls skip their cross-call ordering events and
 // timing marks, and must not grow workspaces: capture after one uncaptured call of the same shape.)
 inline bool capturing(cudaStream_t s) {
@@ -197,15 +230,22 @@ jt_status launch_cfg(LaunchState &st, const jtk::AxisDev &ax, const double *in, 
   // partials (jtk::TermSplit, jtk::ts_reduce), so a latency-bound launch uses more of the GPU
   jtk::TermSplit ts{1, nullptr, 0};
   if (allow_ts && !split && nlines == lay.outer * lay.inner && ax.r >= 2 && batches * 2 <= sms) {
-    const int S = (int)std::min<long long>(ax.r, sms / batches);
+    // (CTAs of the term-split kernel that fit on one SM: two for the one-warp-group kernels capped by JT_WG_GPC)
+    const int bps = C::MINB > 1 ? blocks_per_sm((const void *)ts_kernel<C>(), C::NT, smem) : 1;
+    const int S = (int)std::min<long long>(ax.r, (long long)sms * bps / batches);
     if constexpr (C::CLUSTER_FIT && JT_TS_CLUSTER) {
       // the batch's S CTAs as one thread-block cluster, partials summed through distributed shared memory inside
       // the kernel (jtk::cluster_reduce): one launch, no workspace round trip through L2 / HBM
       auto kern = ts_kernel<C>();
       const int Sc = S > 1 ? cluster_fit((const void *)kern, C::NT, smem, std::min(S, JT_TS_CLUSTER_MAX), (int)batches)
                            : 0;
-      if (Sc > 1) {
-        ts = jtk::TermSplit{Sc, nullptr, 1};
+      if (Sc > 1 && st.mode == 1) {
+        st.q_S = Sc;
+        st.q_cluster = true;
+        return JT_OK;
+      }
+      if (Sc > 1 && st.mode != 2) {
+        ts = jtk::TermSplit{Sc, nullptr, 1, st.in_part, st.in_stride, st.in_S};
         JT_CUDA_TRY(launch_axis_kernel(kern, (unsigned)(batches * Sc), C::NT, smem, s, (unsigned)Sc, ax, in, out,
                                        nlines, lay, ts));
         ++st.launches;
@@ -213,6 +253,11 @@ jt_status launch_cfg(LaunchState &st, const jtk::AxisDev &ax, const double *in, 
       }
     }
     const size_t need = (size_t)S * nlines * ax.n;
+    if (st.mode == 1) {
+      st.q_S = S;
+      st.q_cluster = false;
+      return JT_OK;
+    }
     if (S > 1) {
       if (st.ts_elems < need) {
         if (capturing(s)) return fail(JT_ERR_ARG, "term-split workspace must grow: run the call once before capturing it");
@@ -225,9 +270,15 @@ jt_status launch_cfg(LaunchState &st, const jtk::AxisDev &ax, const double *in, 
           return fail(JT_ERR_ALLOC, "term-split workspace");
         st.ts_elems = need;
       }
-      ts = jtk::TermSplit{S, st.ts_work, 0};
+      ts = jtk::TermSplit{S, st.ts_work, 0, st.in_part, st.in_stride, st.in_S};
     }
   }
+  if (st.mode == 1) {  // (not a term-split launch)
+    st.q_S = 1;
+    st.q_cluster = false;
+    return JT_OK;
+  }
+  if (st.in_S > 0 && ts.S <= 1) return fail(JT_ERR_ARG, "internal: fused partial input on a launch without term split");
   const unsigned grid = ts.S > 1 ? (unsigned)(batches * ts.S) : (unsigned)std::min<long long>(batches, sms);
   if constexpr (C::WG && !JT_WG_LARGE) {  // (only reached for term-split launches: see launch_nmd)
     if (ts.S <= 1) return fail(JT_ERR_ARG, "internal: one-warp-group configuration without term split");
@@ -253,6 +304,10 @@ jt_status launch_cfg(LaunchState &st, const jtk::AxisDev &ax, const double *in, 
   }
   JT_CUDA_TRY(cudaGetLastError());
   ++st.launches;
+  if (ts.S > 1 && st.mode == 2) {  // partials left in the workspace for the next pass to sum
+    st.q_S = ts.S;
+    return JT_OK;
+  }
   if (ts.S > 1) {
     ++st.launches;
     const long long total = nlines * ax.n;
@@ -278,7 +333,7 @@ jt_status launch_nmd(LaunchState &st, const jtk::AxisDev &ax, const double *in, 
                      const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
   using C = jtk::Cfg<N, radix_for<N, MAXR>(), MAXR, INV>;
   using CW = jtk::Cfg<N, radix_ts_of(N, MAXR), MAXR, INV, true>;
-  if constexpr (CW::LG != C::LG || CW::R != C::R) {  // term-split launches: one-warp groups / their own radix
+  if constexpr (JT_TS_WG && (CW::LG != C::LG || CW::R != C::R)) {  // term-split launches: one-warp groups / radix
     const int sms = sm_count();
     if (term_split_applies<CW>(ax, nlines, lay, allow_ts, sms)) {
       jtk::AxisDev axt = ax;

@@ -39,6 +39,9 @@
 #ifndef JT_A1_FOLD_NMIN
 #define JT_A1_FOLD_NMIN 2048  // ... for N >= this (4096^2 forward -2.6 %; 512^3 +0.75 %, 1024 +1.2 %)
 #endif
+#ifndef JT_ZFIRST
+#define JT_ZFIRST 1  // inverse: the first DFT layer skips the thread's zero inputs above R/2 (empty bins > N/2)
+#endif
 #ifndef JT_TW_PREISSUE
 #define JT_TW_PREISSUE 0  // TMEM twiddle chunks loaded one chunk ahead (the next butterfly's during the DFT; r02v: no change)
 #endif
@@ -131,12 +134,26 @@
 #ifndef JT_TS_CLUSTER
 #define JT_TS_CLUSTER 1  // term-split launches as thread-block clusters reducing through DSMEM (no ts_reduce launch)
 #endif
+#ifndef JT_TS_PUSH
+#define JT_TS_PUSH 1  // cluster reduction by bulk copies into the owners' shared memory (else 8-byte remote loads)
+#endif
+#ifndef JT_TS_FUSE
+#define JT_TS_FUSE 0  // term-split axis d-1 pass: partials summed by the next (cluster term-split) pass's loads
+                      // (measured slower: 256^2 30 -> 40 us, the partial loads take more round trips than the
+                      // reduction they replace, r02zk)
+#endif
 #ifndef JT_TS_CLUSTER_MAX
 #define JT_TS_CLUSTER_MAX 16  // largest cluster (non-portable above 8; smaller if the device cannot place it)
 #endif
 #ifndef JT_WG_LARGE
 #define JT_WG_LARGE 0  // N: the one-warp-group configuration (Cfg::WG) for every launch of FFT length N, not only
                        // the term-split ones (0: off)
+#endif
+#ifndef JT_TS_WG
+#define JT_TS_WG 1  // term-split launches of TPL = 16 passes use the one-warp-group configuration (Cfg::WG)
+#endif
+#ifndef JT_WG_GPC
+#define JT_WG_GPC 8  // groups per CTA of the one-warp-group term-split kernels (4: two CTAs per SM)
 #endif
 #ifndef JT_GSPLIT
 #define JT_GSPLIT 2  // group term split (2 or 0 = off): up to this many groups of a term-split CTA share its terms when the batch fits

@@ -346,10 +346,13 @@ def test_repeat_determinism(shape, a, b):
 @pytest.mark.parametrize("shape,a,b", [((512,), (-0.5,), (-0.5,)),           # r = 2: W V mostly outside the ring
                                        ((1000,), (0.5,), (0.5,)),             # r ~ 9, N > n
                                        ((3, 1024), (0.25, -0.5), (-0.3, -0.5)),
-                                       ((7, 256, 5), (0.1, 0.2, 0.3), (0.0, -0.1, 0.2))])
+                                       ((7, 256, 5), (0.1, 0.2, 0.3), (0.0, -0.1, 0.2)),
+                                       ((4096,), (0.3,), (-0.2,)),       # r ~ 22 over 16 CTAs: group term split
+                                       ((2048,), (-0.4,), (0.6,))])
 def test_term_split_launches(shape, a, b):
-    """Few-line launches take the term-split path (rank terms over several CTAs + ts_reduce),
-    including plans with r < k0 / 2 whose dense block is applied outside the term loop (slice 0 only)."""
+    """Few-line launches take the term-split path (rank terms over several CTAs, reduced in a cluster or by ts_reduce,
+    DESIGN.md §6), including plans with r < k0 / 2 whose dense block is applied outside the term loop (split over the
+    slices), and one-line batches whose CTAs deal their terms to two groups (Ctx::gsl)."""
     p = jt.Plan(shape, a, b, 1e-12)
     x = si.gaussian(shape, seed=23)
     assert relerr(gpu_forward(p, x), oracle.forward(x, a, b)) <= TOL

@@ -5,7 +5,8 @@ median / max over CTAs of each phase end (microseconds at the clock the box repo
 
     JT_LIB=paper_1901_07275_b200/libjt_phases.so python tools/phases.py [config ...] > out.txt
 Phases: 1 start (TMEM, twiddles, ring issue)  2 input loads + state  3 batch-start W V block  4 rank terms
-        5 stores  6 TMEM free  7 cluster reduction  8 end.
+        5 stores  6 TMEM free  7-9 cluster reduction (first barrier, remote loads + sums + stores, second barrier)
+        10 reduction done  11 end.
 """
 import ctypes
 import os
@@ -42,7 +43,7 @@ def summarise(text, mhz):
             continue
         t = ln.split()
         rec = dict(kind=t[1], n=t[2], cta=int(t[3][3:]), sm=t[4], terms=int(t[5][5:]), g0=int(t[7]), g1=int(t[9]),
-                   d=[int(v) for v in t[11:19]])
+                   d=[int(v) for v in t[11:22]])
         rows.append(rec)
     if not rows:
         return ["(no PH lines)"]
@@ -60,10 +61,12 @@ def summarise(text, mhz):
         out.append(f"launch {ls[0]['kind']} {ls[0]['n']}: {len(ls)} CTAs, terms {sorted(set(r['terms'] for r in ls))}, "
                    f"globaltimer {g0 / 1e3:.2f} .. {g1 / 1e3:.2f} us (CTA starts spread "
                    f"{(max(r['g0'] for r in ls) - min(r['g0'] for r in ls)) / 1e3:.2f} us)")
-        for i in range(8):
+        names = ["start", "loads", "W V", "terms", "stores", "TMEM free", "cl.bar1", "cl.loads", "cl.bar2", "reduce",
+                 "end"]
+        for i in range(len(ls[0]["d"])):
             vals = sorted(r["d"][i] for r in ls if r["d"][i] > 0)
             if vals:
-                out.append(f"   phase {i + 1} end: median {vals[len(vals) // 2] / mhz:7.2f} us, max {vals[-1] / mhz:7.2f} us")
+                out.append(f"   phase {i + 1:2d} {names[i]:9s} end: median {vals[len(vals) // 2] / mhz:7.2f} us, max {vals[-1] / mhz:7.2f} us")
     return out
 
 
