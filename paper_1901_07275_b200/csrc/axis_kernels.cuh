@@ -70,6 +70,10 @@ struct TermSplit {
   // partial lines are summed through distributed shared memory at the end of the kernel (cluster_reduce): no
   // workspace, no ts_reduce launch
   int cluster;
+  // gsl == 2 (cluster launches only): group term split -- a batch is GPC/2 groups' lines, and each line group is
+  // processed by two groups that deal the CTA's terms between them (Ctx::gsl), so twice the CTAs' worth of terms run
+  // at once where a one-wave cluster grid cannot take more slices (256^2: 3 -> 2 terms per group)
+  int gsl = 1;
   // in_S > 0 (term-split launches only): the input is the sum, in slice order, of in_S arrays at in_part + s in_stride
   // (the previous pass's partials, not reduced by a launch of their own: the reduction fused into this pass's loads)
   const double *in_part = nullptr;
@@ -849,12 +853,16 @@ struct Ctx {
   Ring<C> ring;
   long long nbatch, bt0, btstep;
   int slice = 0, S = 1, l0 = 0, l1 = 0;
-  // Group term split (term-split cluster launches whose batch fits in one group's LG lines, e.g. a 1D transform):
-  // the CTA's terms are dealt round-robin to gsl groups, which all process the lines of group 0 (lgrp) and keep
-  // separate partials (summed by cluster_reduce); groups grp >= gsl, and groups whose lines are all past the end
-  // (dead), only take part in the factor ring.
-  int gsl = 1, lgrp = 0;
+  // Group term split (TermSplit::gsl == 2, chosen by the launch): a batch is GU = GPC/2 groups' lines; group grp works
+  // on line group lgrp = grp % GU as slice group sg = grp / GU, the CTA's terms dealt round-robin to the gsl (<= 2)
+  // slice groups, each keeping its own partials (summed by cluster_reduce); groups sg >= gsl, and groups whose lines
+  // are all past the end (dead), only take part in the factor ring.
+  int gsl = 1, lgrp = 0, sg = 0, GU = C::GPC;
   bool dead = false;
+  // first line of this group in batch bt
+  __device__ __forceinline__ long long batch_line(long long bt) const {
+    return (bt * (TSPLIT ? GU : C::GPC) + lgrp) * C::LG + line;
+  }
   const double2 *gv, *gu;
   __device__ __forceinline__ Ctx(char *smem, const AxisDev &ax, long long nlines, const TermSplit &ts) {
     grp = threadIdx.x / C::GT;
@@ -877,7 +885,8 @@ struct Ctx {
     alow = reinterpret_cast<double *>(gb + C::SLOTS * C::XB);
     priv = alow + K0MAX * C::LG;
     vred = priv + C::PSLOTS * C::GT;
-    nbatch = (nlines + C::GPC * C::LG - 1) / (C::GPC * C::LG);
+    if (TSPLIT && ts.gsl == 2) GU = C::GPC / 2;
+    nbatch = (nlines + (long long)GU * C::LG - 1) / ((long long)GU * C::LG);
     S = TSPLIT ? ts.S : 1;
     long long mine;
     if (TSPLIT) {  // one (batch, term slice) per CTA
@@ -895,13 +904,13 @@ struct Ctx {
       mine = blockIdx.x < nbatch ? (nbatch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     }
     lgrp = grp;
-    if (TSPLIT && ts.cluster && JT_GSPLIT && C::GPC > 1) {
-      const long long lines_b = nlines - bt0 * C::GPC * C::LG;
-      if (lines_b <= C::LG) gsl = min(min(C::GPC, JT_GSPLIT), max(l1 - l0, 1));
-      if (gsl > 1) lgrp = 0;
+    if (TSPLIT && ts.gsl == 2) {
+      lgrp = grp % GU;
+      sg = grp / GU;
+      gsl = min(2, max(l1 - l0, 1));
     }
     // (term-split launches only: one batch per CTA; the persistent launches keep the plain loop)
-    dead = TSPLIT && ((gsl > 1 && grp >= gsl) || (gsl == 1 && (bt0 * C::GPC + grp) * C::LG >= nlines));
+    dead = TSPLIT && (sg >= gsl || (bt0 * GU + lgrp) * C::LG >= nlines);
     ring.l0 = l0;
     ring.rs = l1 - l0 > 0 ? l1 - l0 : 1;
     ring.total = mine * (l1 - l0) * (C::SUB ? C::NSUB : 1);
@@ -995,17 +1004,17 @@ struct Ctx {
   __device__ __forceinline__ int kv0(int kin, int k0) const {
     if (!TSPLIT) return kin;
     const int a = kin + (int)((long long)(k0 - kin) * slice / S), b = kin + (int)((long long)(k0 - kin) * (slice + 1) / S);
-    return gsl > 1 && grp < gsl ? a + (b - a) * grp / gsl : a;
+    return gsl > 1 && sg < gsl ? a + (b - a) * sg / gsl : a;
   }
   __device__ __forceinline__ int kv1(int kin, int k0) const {
     if (TSPLIT && dead) return kv0(kin, k0);
     if (!TSPLIT) return k0;
     const int a = kin + (int)((long long)(k0 - kin) * slice / S), b = kin + (int)((long long)(k0 - kin) * (slice + 1) / S);
-    return gsl > 1 ? a + (b - a) * (grp + 1) / gsl : b;
+    return gsl > 1 ? a + (b - a) * (sg + 1) / gsl : b;
   }
   // does this group process rank term l (of this CTA's l0 .. l1 - 1)?
   __device__ __forceinline__ bool mine(int l) const {
-    return !TSPLIT || (!dead && (gsl == 1 || (l - l0) % gsl == grp));
+    return !TSPLIT || (!dead && (gsl == 1 || (l - l0) % gsl == sg));
   }
   __device__ __forceinline__ const double2 *vfac(long long seq, int l) const {
     if constexpr (C::STAGED) return ring.v(seq);
@@ -1175,14 +1184,15 @@ __device__ __forceinline__ void cluster_reduce(double *out, const TermSplit &ts,
   unsigned rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const long long bt = blockIdx.x / ts.S;
-  const long long L0 = bt * C::GPC * C::LG;
-  const long long lines = min((long long)C::GPC * C::LG, nlines - L0);
+  const int GU = ts.gsl == 2 ? C::GPC / 2 : C::GPC;  // line groups per batch
+  const long long L0 = bt * GU * C::LG;
+  const long long lines = min((long long)GU * C::LG, nlines - L0);
   const long long E = lines * n;
   const uint32_t base = smem_u32(cluster_part<C>());
   const long long e1 = (rank + 1) * E / ts.S;
-  // (group term split, Ctx::gsl: CTA t keeps gsl_t partials of the batch's lines, group g's at g LG lines)
-  const bool gs = JT_GSPLIT > 1 && C::GPC > 1 && lines <= C::LG;
-  const uint32_t gstride = (uint32_t)(C::LG * n * 8);
+  // (group term split, Ctx::gsl: CTA t keeps gsl_t partials of the batch's lines, slice group g's at g GU LG lines)
+  const bool gs = ts.gsl == 2;
+  const uint32_t gstride = (uint32_t)(GU * C::LG * n * 8);
   unsigned two = 0;  // bit t: CTA t holds two partials (Ctx::gsl == 2: at least two terms)
   if (gs)
     for (int t = 0; t < ts.S; ++t)
@@ -1260,10 +1270,11 @@ __device__ __forceinline__ bool cluster_reduce_push(double *out, const TermSplit
   extern __shared__ __align__(128) char smem_raw[];
   const int S = ts.S;
   const long long bt = blockIdx.x / S;
-  const long long L0 = bt * C::GPC * C::LG;
-  const int lines = (int)min((long long)C::GPC * C::LG, nlines - L0);
+  const int GU = ts.gsl == 2 ? C::GPC / 2 : C::GPC;  // line groups per batch
+  const long long L0 = bt * GU * C::LG;
+  const int lines = (int)min((long long)GU * C::LG, nlines - L0);
   const int E = lines * n;
-  const bool gs = JT_GSPLIT > 1 && C::GPC > 1 && lines <= C::LG;
+  const bool gs = ts.gsl == 2;
   unsigned two = 0;
   if (gs)
     for (int t = 0; t < S; ++t)
@@ -1272,7 +1283,7 @@ __device__ __forceinline__ bool cluster_reduce_push(double *out, const TermSplit
   const int RS = ((E + S - 1) / S + 3) & ~1;  // receive slot stride (doubles, even) >= every range + 1
   const int recv_bytes = slots * RS * 8;
   // (uniform over the cluster: every CTA takes the same branch)
-  if (recv_bytes + 16 > C::HDR_BYTES || (gs && (C::LG * n) % 2 != 0)) return false;
+  if (recv_bytes + 16 > C::HDR_BYTES || (gs && (GU * C::LG * n) % 2 != 0)) return false;
   double *recv = reinterpret_cast<double *>(smem_raw);
   uint64_t *mbar = reinterpret_cast<uint64_t *>(smem_raw + ((recv_bytes + 15) & ~15));
   unsigned rank;
@@ -1308,7 +1319,7 @@ __device__ __forceinline__ bool cluster_reduce_push(double *out, const TermSplit
                    "r"(src), "r"(bytes), "r"(mb)
                    : "memory");
     if ((two >> rank) & 1u) {  // the second group's partial (Ctx::gsl == 2) into slot S + rank
-      const uint32_t src2 = smem_u32(cluster_part<C>() + C::LG * n + at);
+      const uint32_t src2 = smem_u32(cluster_part<C>() + GU * C::LG * n + at);
       uint32_t dst2;
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst2) : "r"(smem_u32(recv + (S + rank) * RS)), "r"(t));
       if (bytes)
@@ -1364,7 +1375,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
   // (term split, latency-bound: the batch's input lines requested into L2 while the previous kernel finishes -- only a
   // cache hint, so it may precede the dependency wait: L2 is the point of coherence)
   if constexpr (TSPLIT && JT_PDL_PREFETCH)
-    prefetch_line<C, SPLIT>(in, lay, (cx.bt0 * C::GPC + cx.lgrp) * LG + cx.line, nlines, cx.vt, ax.n);
+    prefetch_line<C, SPLIT>(in, lay, cx.batch_line(cx.bt0), nlines, cx.vt, ax.n);
   pdl_wait();  // (the prologue above touches only plan data: the arrays are the previous kernel's)
   phs.mark(1);
   const int n = ax.n, k0 = ax.k0;
@@ -1378,7 +1389,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
 
   long long seq = 0;
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
-    const long long L = (bt * C::GPC + cx.lgrp) * LG + line;
+    const long long L = cx.batch_line(bt);
     const bool live = L < nlines && (!TSPLIT || !cx.dead);
     const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
     const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs, lay.out_peer, lay.out_row);
@@ -1642,7 +1653,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
   // (term split, latency-bound: the batch's input lines requested into L2 while the previous kernel finishes -- only a
   // cache hint, so it may precede the dependency wait: L2 is the point of coherence)
   if constexpr (TSPLIT && JT_PDL_PREFETCH)
-    prefetch_line<C, SPLIT>(in, lay, (cx.bt0 * C::GPC + cx.lgrp) * LG + cx.line, nlines, cx.vt, ax.n);
+    prefetch_line<C, SPLIT>(in, lay, cx.batch_line(cx.bt0), nlines, cx.vt, ax.n);
   pdl_wait();  // (the prologue above touches only plan data: the arrays are the previous kernel's)
   phs.mark(1);
   const int n = ax.n, k0 = ax.k0;
@@ -1658,7 +1669,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
 
   long long seq = 0;
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
-    const long long L = (bt * C::GPC + cx.lgrp) * LG + line;
+    const long long L = cx.batch_line(bt);
     const bool live = L < nlines && (!TSPLIT || !cx.dead);
     const LineAddr<SPLIT> ia(live ? L : 0, lay.ostride, lay.inner, n, lay.in_cs);
     const LineAddr<SPLIT> oa(live ? L : 0, lay.ostride, lay.inner, n, lay.out_cs, lay.out_peer, lay.out_row);

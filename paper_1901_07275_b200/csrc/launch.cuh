@@ -245,8 +245,25 @@ jt_status launch_cfg(LaunchState &st, const jtk::AxisDev &ax, const double *in, 
         return JT_OK;
       }
       if (Sc > 1 && st.mode != 2) {
-        ts = jtk::TermSplit{Sc, nullptr, 1, st.in_part, st.in_stride, st.in_S};
-        JT_CUDA_TRY(launch_axis_kernel(kern, (unsigned)(batches * Sc), C::NT, smem, s, (unsigned)Sc, ax, in, out,
+        // group term split (jtk::TermSplit::gsl): batches of GPC/2 groups' lines, two groups per line group dealing
+        // the terms, when that needs fewer rounds of terms per group than the plain split (one-wave clusters)
+        long long nb = batches;
+        int Sg = Sc, gsl = 1;
+        if constexpr (JT_GSPLIT >= 2 && C::GPC % 2 == 0) {
+          const long long b2 = (nlines + lines_per_batch / 2 - 1) / (lines_per_batch / 2);
+          const int S2 = (int)std::min<long long>(ax.r, (long long)sms * bps / b2);
+          const int Sc2 = S2 > 1 ? cluster_fit((const void *)kern, C::NT, smem, std::min(S2, JT_TS_CLUSTER_MAX), (int)b2)
+                                 : 0;
+          const int rounds1 = (ax.r + Sc - 1) / Sc;
+          const int rounds2 = Sc2 > 1 ? ((ax.r + Sc2 - 1) / Sc2 + 1) / 2 : rounds1;
+          if (rounds2 < rounds1) {
+            nb = b2;
+            Sg = Sc2;
+            gsl = 2;
+          }
+        }
+        ts = jtk::TermSplit{Sg, nullptr, 1, gsl, st.in_part, st.in_stride, st.in_S};
+        JT_CUDA_TRY(launch_axis_kernel(kern, (unsigned)(nb * Sg), C::NT, smem, s, (unsigned)Sg, ax, in, out,
                                        nlines, lay, ts));
         ++st.launches;
         return JT_OK;
@@ -270,7 +287,7 @@ jt_status launch_cfg(LaunchState &st, const jtk::AxisDev &ax, const double *in, 
           return fail(JT_ERR_ALLOC, "term-split workspace");
         st.ts_elems = need;
       }
-      ts = jtk::TermSplit{S, st.ts_work, 0, st.in_part, st.in_stride, st.in_S};
+      ts = jtk::TermSplit{S, st.ts_work, 0, 1, st.in_part, st.in_stride, st.in_S};
     }
   }
   if (st.mode == 1) {  // (not a term-split launch)

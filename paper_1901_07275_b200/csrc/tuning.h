@@ -46,7 +46,8 @@
 #define JT_TW_PREISSUE 0  // TMEM twiddle chunks loaded one chunk ahead (the next butterfly's during the DFT; r02v: no change)
 #endif
 #ifndef JT_TWT_INV32
-#define JT_TWT_INV32 0  // ... also for the radix-32 inverse (measured 2 % slower)
+#define JT_TWT_INV32 1  // ... also for the radix-32 inverse (round 1: 2 % slower; after the round-2 changes 512^3
+                        // inverse 17.84 -> 17.75 ms, 128^3 +0.4 %, r02zn)
 #endif
 #ifndef JT_TWT_LARGE
 #define JT_TWT_LARGE 1  // N > 1024: one TMEM twiddle copy per lane quadrant (4096^2 forward 4.05 -> 3.81 ms)
