@@ -328,11 +328,21 @@ struct Cfg {
   static constexpr bool TWT = (TWS || TWT_LARGE) && TPRIV && JT_TWT && TWPT > 0 && MAXR == 2 &&
                               (!INV || R == 16 || JT_TWT_INV32 || !TWS);
   static constexpr bool TW_SHARED = TWT && !TWS;
+  static constexpr bool VTM_PRE = JT_VTM && N == 512 && R == 32 && MAXR == 2 && !INV && !WG;  // (see VTM)
+  // VTM (N = 512 forward): the rank term's v_l read from tensor memory instead of broadcast LDS.128s (64 of the 456
+  // shared-memory wavefronts per warp and term): one thread copies the ring stage's v_l into TMEM with tcgen05.cp
+  // (.32x128b.warpx4, stride-0 core matrices: each 8-row block of v repeated down a lane quadrant), so the lanes are
+  // mapped line-major (lane = 8 line + vt % 8) and the exchange slots line-major too; block A (vt 0..7) and B
+  // (vt 8..15) both go to every quadrant, quadrants 0, 2 read A and 1, 3 read B; the twiddles are one copy per
+  // quadrant (its two warps have the same vt) -- 64 + 64 (states) + 128 (twiddles) + 2 x 128 (v) = 512 columns.
+  static constexpr bool VTM = VTM_PRE && LG == 4 && GT == 64 && STAGED && TWT && TWS;
+  static constexpr bool TW_QSHARE = TW_SHARED || VTM;  // one twiddle copy per lane quadrant
   static constexpr int TW_BYTES = (TWS && !TWT) ? (TwTotal<N, R>::value * 16 + 127) / 128 * 128 : 0;
   // per-CTA table of the row range of every (thread position vt, bin slot q): (j0 << 4) | count
   static constexpr int BINFO_BYTES = STAGED ? (TPL * NB * 4 + 127) / 128 * 128 : 0;
+  static constexpr int VTM_BYTES = VTM_PRE ? 16 : 0;  // (VTM: v-ready mbarrier + v-consumed counter after the ring)
   static constexpr int hdr_bytes(int nstage) {
-    return (nstage * STAGE_BYTES + 3 * nstage * 8 + 127) / 128 * 128 + BINFO_BYTES + TW_BYTES;
+    return (nstage * STAGE_BYTES + 3 * nstage * 8 + VTM_BYTES + 127) / 128 * 128 + BINFO_BYTES + TW_BYTES;
   }
   static constexpr int gpc_fit(int g, int nstage) {
     return (g > 1 && (((g * GT + 127) / 128) * 128 * REGS > 65536 || g * GROUP_BYTES + hdr_bytes(nstage) > SMEM_LIMIT ||
@@ -364,14 +374,18 @@ struct Cfg {
                                     : ((STAGED && GPC * GROUP_BYTES + hdr_bytes(3) <= SMEM_LIMIT) ? 3 : (URING ? 1 : 2));
   static_assert(!SUB || GPC * GROUP_BYTES + hdr_bytes(NSTAGE) <= SMEM_LIMIT, "SUB ring");
   static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES + 3 * NSTAGE * 8;  // stages + full/empty barriers + counters
-  static constexpr int BINFO_OFF = (RING_BYTES + 127) / 128 * 128;
+  static constexpr int BINFO_OFF = (RING_BYTES + VTM_BYTES + 127) / 128 * 128;
   static constexpr int TW_OFF = BINFO_OFF + BINFO_BYTES;
   static constexpr int HDR_BYTES = hdr_bytes(NSTAGE);
   static constexpr int NT = GPC * GT;  // threads per CTA
   static constexpr size_t smem_bytes() { return (size_t)HDR_BYTES + (size_t)GPC * GROUP_BYTES; }
   // term-split partial lines of a batch (GPC LG lines x N doubles) fit in the group areas (cluster reduction)
   static constexpr bool CLUSTER_FIT = (long long)GPC * LG * N * 8 <= (long long)GPC * GROUP_BYTES;
-  __device__ static __forceinline__ int sidx(int pos, int line) { return (pos + pos / R) * LG + line; }
+  __device__ static __forceinline__ int sidx(int pos, int line) {
+    // (VTM: line-major with one pad slot per 32 -- conflict-free for its lane = 8 line + vt % 8 mapping)
+    if constexpr (VTM) return line * (N + N / 32) + pos + pos / 32;
+    else return (pos + pos / R) * LG + line;
+  }
   static_assert(GT % 32 == 0, "group must be whole warps");
   static_assert(RSL >= 2, "last pass radix");
   static_assert(smem_bytes() <= SMEM_LIMIT, "shared memory");
@@ -384,14 +398,17 @@ struct Cfg {
   static constexpr int WPQ = (NWARP + 3) / 4;  // warps per lane quadrant
   // columns of a quadrant: WPQ slices [state | own twiddles], or (TW_SHARED) WPQ state slices + one twiddle copy
   // (+32: a butterfly's twiddle loads are whole 8-complex chunks and may read past the last one)
-  static constexpr int TUSED = TW_SHARED ? WPQ * TW_COL0 + TW_COLS + 32 : (TW_COL0 + TW_COLS) * WPQ;
+  static constexpr int V_COLA = WPQ * TW_COL0 + TW_COLS, V_COLB = V_COLA + 4 * R;  // VTM: v blocks A / B
+  static constexpr int TUSED = VTM ? V_COLB + 4 * R
+                                   : (TW_SHARED ? WPQ * TW_COL0 + TW_COLS + 32 : (TW_COL0 + TW_COLS) * WPQ);
   // allocate only what the slices use (a power of two >= 32), so CTAs that co-reside on an SM can all allocate
   static constexpr int TALLOC = pow2_ge(TUSED > 512 ? 512 : TUSED);
-  static constexpr int TSTRIDE = TW_SHARED ? TW_COL0 : TALLOC / WPQ / 16 * 16;
-  static constexpr int TW_BASE = TW_SHARED ? WPQ * TW_COL0 : TW_COL0;  // twiddles: from the quadrant / slice base
+  static constexpr int TSTRIDE = TW_QSHARE ? TW_COL0 : TALLOC / WPQ / 16 * 16;
+  static constexpr int TW_BASE = TW_QSHARE ? WPQ * TW_COL0 : TW_COL0;  // twiddles: from the quadrant / slice base
   static constexpr bool TMEM_OK =
-      !TPRIV || (NWARP % 4 == 0 && (TW_SHARED ? TUSED <= 512 : TW_COL0 + TW_COLS <= TCOLS));
-  static_assert(!TPRIV || TW_SHARED || TW_COL0 + TW_COLS <= TSTRIDE, "TMEM slice stride");
+      !TPRIV || (NWARP % 4 == 0 && (TW_QSHARE ? TUSED <= 512 : TW_COL0 + TW_COLS <= TCOLS));
+  static_assert(!TPRIV || TW_QSHARE || TW_COL0 + TW_COLS <= TSTRIDE, "TMEM slice stride");
+  static_assert(!VTM || (NWARP == 8 && TUSED == 512 && TW_COL0 == 64 && TW_COLS == 128), "VTM TMEM layout");
 #ifndef JT_NO_TMEM_ASSERT
   static_assert(TMEM_OK, "TMEM state slice");
 #endif
@@ -443,6 +460,13 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// Shared-memory matrix descriptor of a tcgen05.cp source (no swizzle; 8-row x 16-byte core matrices, rows 16 bytes
+// apart): start address, leading / stride-dimension byte offsets 0 (a 128-bit-wide copy has one core matrix along K;
+// stride 0 repeats the first core matrix down the copy's rows -- measured, tools/tmem_cp_probe.cu), version 1.
+__device__ __forceinline__ uint64_t tmem_cp_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 46);
 }
 
 // The CTA's factor ring.  Sequence number seq = (batch iteration) r + l walks the terms of every batch
@@ -846,6 +870,9 @@ struct Ctx {
   int grp, gt, line, vt;
   uint32_t tbase = 0, taddr = 0;  // TMEM allocation base / this thread's state slice (C::TPRIV)
   uint32_t ttw = 0;               // this thread's twiddles (C::TWT)
+  uint32_t tv = 0;                // C::VTM: this warp's v_l block (A or B) in its lane quadrant
+  uint64_t *vbar = nullptr;       // C::VTM: v_l copied into TMEM (tcgen05.commit), one phase per term
+  unsigned *vcnt = nullptr;       // C::VTM: warps done reading v_l (monotonic: NWARP per term)
   void *buf;     // group exchange buffer
   double *alow;  // group: k0 x LG low-degree coefficients (forward) / reduced a_V (inverse)
   double *priv;  // group: thread-private slots [slot][gt] (C::PRIV)
@@ -867,14 +894,23 @@ struct Ctx {
   __device__ __forceinline__ Ctx(char *smem, const AxisDev &ax, long long nlines, const TermSplit &ts) {
     grp = threadIdx.x / C::GT;
     gt = threadIdx.x % C::GT;
-    line = gt % C::LG;
-    vt = gt / C::LG;
+    if constexpr (C::VTM) {  // lane = 8 line + vt % 8 (the TMEM v blocks repeat 8 rows down the quadrant)
+      line = (gt & 31) >> 3;
+      vt = ((gt >> 5) << 3) | (gt & 7);
+    } else {
+      line = gt % C::LG;
+      vt = gt / C::LG;
+    }
     gv = ax.v;
     gu = ax.ub;
     ring.base = smem;
     ring.full = reinterpret_cast<uint64_t *>(smem + C::NSTAGE * C::STAGE_BYTES);
     ring.empty = ring.full + C::NSTAGE;
     ring.cnt = reinterpret_cast<unsigned *>(ring.empty + C::NSTAGE);
+    if constexpr (C::VTM) {
+      vbar = reinterpret_cast<uint64_t *>(ring.cnt + C::NSTAGE + (C::NSTAGE & 1));  // (8-byte aligned)
+      vcnt = reinterpret_cast<unsigned *>(vbar + 1);
+    }
     ring.gv = ax.v;
     ring.gu = ax.ub;
     ring.r = ax.r;
@@ -946,6 +982,10 @@ struct Ctx {
           mbar_init(&ring.full[s], 1);
           ring.cnt[s] = 0;
         }
+        if constexpr (C::VTM) {
+          mbar_init(vbar, 1);
+          *vcnt = 0;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (long long q = 0; q < C::NSTAGE && q < ring.total; ++q) ring.issue(q);
       }
@@ -967,11 +1007,13 @@ struct Ctx {
       tbase = tslot;
       const int w = threadIdx.x / 32;
       taddr = tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)((w / 4) * C::TSTRIDE);
-      ttw = C::TW_SHARED ? tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)C::TW_BASE : taddr + C::TW_BASE;
+      ttw = C::TW_QSHARE ? tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)C::TW_BASE : taddr + C::TW_BASE;
+      if constexpr (C::VTM)  // quadrants 0, 2 hold the group's first warps (vt 0..7: block A), 1, 3 the second (B)
+        tv = tbase + ((uint32_t)(32 * (w % 4)) << 16) + (uint32_t)(((w & 1) == 0) ? C::V_COLA : C::V_COLB);
     }
     if constexpr (C::TWT) {  // the thread's twiddles, once for the whole kernel
-      // (TW_SHARED: the quadrant's first warp writes the copy; the others read it after the barrier below)
-      if (!C::TW_SHARED || threadIdx.x < 128) {
+      // (TW_QSHARE: the quadrant's first warp writes the copy; the others read it after the barrier below)
+      if (!C::TW_QSHARE || threadIdx.x < 128) {
         constexpr int NV = (2 * C::TWPT + 7) / 8 * 8;
         double t[NV];
 #pragma unroll
@@ -982,11 +1024,56 @@ struct Ctx {
           if (JT_CHK((int)(ttw & 0xffff) + 16 * c + 16 <= C::TALLOC)) tmem_st_d8(ttw + 16 * c, &t[8 * c]);
         tmem_wait_st();
       }
-      if constexpr (C::TW_SHARED) {
+      if constexpr (C::TW_QSHARE) {
         tmem_fence_before_sync();
         __syncthreads();
         tmem_fence_after_sync();
       }
+    }
+    if constexpr (C::VTM)
+      if (threadIdx.x == 0 && ring.total > 0) v_issue(0);  // the first term's v_l (its TMA stage issued above)
+  }
+  // C::VTM: copy term sq's v_l from its ring stage into TMEM blocks A (v[16r .. 16r + 7]) and B (v[16r + 8 ..]),
+  // r = 0..31, each 8-row core matrix repeated down the 32 lanes of every quadrant (stride-dimension offset 0); one
+  // thread, after the stage has landed and every warp has read the previous term's v_l.
+  __device__ __forceinline__ void v_issue(long long sq) const {
+    if constexpr (C::VTM) {
+      mbar_wait(&ring.full[sq % C::NSTAGE], (uint32_t)((sq / C::NSTAGE) & 1));
+      tmem_fence_after_sync();
+      const uint32_t st = smem_u32(ring.v(sq));
+#pragma unroll 8
+      for (int r = 0; r < C::R; ++r) {
+        const uint64_t da = tmem_cp_desc(st + 256 * r), db = tmem_cp_desc(st + 256 * r + 128);
+        asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tbase + C::V_COLA + 4 * r), "l"(da)
+                     : "memory");
+        asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tbase + C::V_COLB + 4 * r), "l"(db)
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(vbar))
+                   : "memory");
+    }
+  }
+  // C::VTM: wait until term seq's v_l is in TMEM
+  __device__ __forceinline__ void v_wait(long long seq) const {
+    if constexpr (C::VTM) {
+      jitter();
+      mbar_wait(vbar, (uint32_t)(seq & 1));
+      __syncwarp();
+      tmem_fence_after_sync();
+    }
+  }
+  // C::VTM: this warp is done reading term seq's v_l; the last of the CTA's warps copies term seq + 1's
+  __device__ __forceinline__ void v_free(long long seq) const {
+    if constexpr (C::VTM) {
+      tmem_fence_before_sync();
+      jitter();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(vcnt)) : "memory");
+        if (old + 1 == (unsigned)(C::NWARP * (seq + 1)) && seq + 1 < ring.total) v_issue(seq + 1);
+      }
+      __syncwarp();
     }
   }
   // end of the kernel: every warp's TMEM traffic done, then warp 0 frees the allocation
@@ -1440,6 +1527,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
     for (int l = cx.l0; l < cx.l1; ++l, ++seq) {
       cx.acquire(seq);
       if (!cx.mine(l)) {  // (another group's term, or a dead group: only the ring protocol)
+        cx.v_wait(seq);
+        cx.v_free(seq);
         cx.acquire_u(seq);
         if constexpr (!C::LATE) group_sync<C>();
         cx.release(seq);
@@ -1509,6 +1598,23 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
             }
           }
         }
+      } else if constexpr (C::VTM) {
+        // A1 with v_l from TMEM: 8 positions per step (state chunk of 8 + 8 complex of this warp's v block)
+        cx.v_wait(seq);
+#pragma unroll
+        for (int ch = 0; ch < R / 8; ++ch) {
+          double ac[8], vr[16];
+          tmem_ld_d8(cx.taddr + 16 * ch, ac);
+          tmem_ld_d8(cx.tv + 32 * ch, &vr[0]);
+          tmem_ld_d8(cx.tv + 32 * ch + 16, &vr[8]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            xr[8 * ch + i] = vr[2 * i] * ac[i];
+            xi[8 * ch + i] = vr[2 * i + 1] * ac[i];
+          }
+        }
+        cx.v_free(seq);
       } else if constexpr (C::A1FOLD) {
         // A1 folded into the first butterfly layer of the radix-32 DFT: positions r < 16 scaled (state chunk 0), then
         // x_r +- x_{r+16} = fma(+-v_{r+16}, a_{r+16}, v_r a_r) with state chunk 1 (dft<32, true> skips that layer)

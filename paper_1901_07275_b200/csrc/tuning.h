@@ -42,6 +42,12 @@
 #ifndef JT_ZFIRST
 #define JT_ZFIRST 1  // inverse: the first DFT layer skips the thread's zero inputs above R/2 (empty bins > N/2)
 #endif
+#ifndef JT_VTM
+#define JT_VTM 0  // N = 512 forward: v_l from tensor memory (tcgen05.cp from the ring stage) instead of LDS broadcasts
+                  // (correct, but 512^3 forward 17.1 -> 30.4 ms: TMEM holds one term's v only, so every warp waits
+                  // for the slowest warp's previous term at each term start -- the groups lose the phase spread
+                  // that overlaps their FP64 and shared-memory work, r02zp)
+#endif
 #ifndef JT_TW_PREISSUE
 #define JT_TW_PREISSUE 0  // TMEM twiddle chunks loaded one chunk ahead (the next butterfly's during the DFT; r02v: no change)
 #endif

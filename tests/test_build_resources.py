@@ -1,6 +1,8 @@
 """Resource usage of the built sm_100a kernels (CPU: cuobjdump on the in-tree libjt.so, no GPU needed).
-The bench workload's kernels (512^3: the N = 512, radix-32 forward and inverse over plain layouts) must not spill:
-a register-allocation regression there shows up as local-memory traffic in the hot loop."""
+The bench workload's kernel (512^3: the N = 512, radix-32 forward over plain layouts) must not spill: a
+register-allocation regression there shows up as local-memory traffic in the hot loop.  Its inverse
+may keep a few bytes of stack: with its twiddles in TMEM (tuning.h JT_TWT_INV32) ptxas spills 16 bytes and the
+pass is still 0.5 % faster than with the shared-memory twiddle table (profiles/ab_r02zn.txt)."""
 import os
 import re
 import shutil
@@ -34,7 +36,7 @@ def test_bench_kernels_do_not_spill(direction, inv):
     hits = [v for k, v in res.items() if key in k]
     assert len(hits) == 1, key
     r = hits[0]
-    assert r["REG"] <= 255 and r["STACK"] == 0 and r["LOCAL"] == 0, r
+    assert r["REG"] <= 255 and r["STACK"] <= (0 if direction == "fwd" else 32) and r["LOCAL"] == 0, r
 
 
 def test_every_axis_kernel_fits_the_register_file():
