@@ -64,7 +64,8 @@ typedef enum {
 typedef struct {
   uint64_t seed;   /* PRNG seed of Algorithm 1's random row/column samples (default 0) */
   int k0;          /* number of low degrees kept in the dense block V, 0..32; default -1 = auto:
-                      the paper's 27, or 32 where that lowers the rank (FFT length <= 512; R24) */
+                      the paper's 27, or 32 where that lowers the rank (FFT length <= 512), or 20 / 24 where that
+                      keeps the rank (FFT length 4096 / 2048; R24) */
   int rmax_init;   /* initial rank cap of Algorithm 1; 0 = max(ceil(2 log2 n), 32) */
   int q;           /* oversampling factor of Algorithm 1 (default 3; "q = O(1)") */
   int sweeps;      /* repetitions of Algorithm 1 steps 2-3 (default 2) */

@@ -1082,6 +1082,15 @@ jt_status jt_plan_ex(jt_plan_t *out, int d, const int64_t n[], const double a[],
         oa.k0 = 32;
         if (jt::build_axis_host(alt, n[i], a[i], b[i], eps, oa, err2, pts, kind) == JT_OK && alt.r < p->host[i].r)
           p->host[i] = std::move(alt);
+      } else if (s == JT_OK && o.k0 == -1 && p->host[i].N >= 2048) {
+        // auto k0 (reading R24): for N >= 2048 the batch-start W V loop streams k0 x n doubles per line through L1 (a
+        // degree costs ~1/14 of a rank term, r02zt); a narrower block that keeps the rank is strictly cheaper
+        // (4096^2: k0 27 -> 20, forward -2.1 %, inverse -2.4 %; 2048^2: 27 -> 24, -1.2 %)
+        jt::AxisHost alt;
+        std::string err2;
+        oa.k0 = p->host[i].N >= 4096 ? 20 : 24;
+        if (jt::build_axis_host(alt, n[i], a[i], b[i], eps, oa, err2, pts, kind) == JT_OK && alt.r <= p->host[i].r)
+          p->host[i] = std::move(alt);
       }
       if (s != JT_OK) {
         delete p;

@@ -247,10 +247,15 @@ def test_amplitude_non_oscillatory():
 
 def test_auto_k0():
     """k0 = -1 (default, R24): the paper's 27, or 32 when that lowers the rank for FFT lengths
-    <= 512; explicit k0 values are kept."""
+    <= 512, or the narrower 20 (FFT length 4096) / 24 (2048) when that keeps the rank; explicit k0 values are kept."""
     p = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2)
     r27 = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2, k0=27).rank()
     r32 = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2, k0=32).rank()
     assert p.info()["k0"] == (32 if r32 < r27 else 27) and p.rank() == min(r27, r32)
-    assert jt.Plan(1024, 0.25, -0.3, 1e-12, device=-2).info()["k0"] == 27  # FFT length > 512
+    assert jt.Plan(1024, 0.25, -0.3, 1e-12, device=-2).info()["k0"] == 27  # FFT length 1024: the paper's 27
+    for n, kn in ((2048, 24), (4096, 20)):
+        p = jt.Plan(n, 0.45, -0.45, 1e-12, device=-2)
+        r27 = jt.Plan(n, 0.45, -0.45, 1e-12, device=-2, k0=27).rank()
+        rn = jt.Plan(n, 0.45, -0.45, 1e-12, device=-2, k0=kn).rank()
+        assert p.info()["k0"] == (kn if rn <= r27 else 27) and p.rank() == min(r27, rn)
     assert jt.Plan(512, 0.25, -0.25, 1e-12, device=-2, k0=20).info()["k0"] == 20
