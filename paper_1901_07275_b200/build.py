@@ -53,9 +53,11 @@ UNITS = ["launch_4096", "launch_512", "launch_2048", "launch_1024", "launch_256"
          "launch_32", "launch_16", "jt_api"]
 
 
-def build(verbose_ptxas: bool = False, out: str = LIB, defines=(), tag: str = "", checks: bool = True) -> str:
-    """Compile libjt.so (or a variant: `out` path, extra -D `defines`, object-file `tag`); with `checks` (default,
-    only for the default build) also libjt_checks.so.  All translation units compile in parallel."""
+def build(verbose_ptxas: bool = False, out: str = LIB, defines=(), tag: str = "", checks: bool = True,
+          extra=()) -> str:
+    """Compile libjt.so (or a variant: `out` path, extra -D `defines`, extra nvcc flags `extra`, object-file `tag`);
+    with `checks` (default, only for the default build) also libjt_checks.so.  All translation units compile in
+    parallel."""
     nvcc = _nvcc()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     # object files outside the repository (they need not travel to the GPU box with the libraries)
@@ -63,11 +65,11 @@ def build(verbose_ptxas: bool = False, out: str = LIB, defines=(), tag: str = ""
     os.makedirs(build_dir, exist_ok=True)
     plan_o = os.path.join(build_dir, "plan.o")
     # (compressed fatbins: one translation unit per FFT length repeats the line tables, 45 -> ~15 MB per library)
-    base = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xfatbin=-compress-all", *inc]
+    base = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xfatbin=-compress-all", *inc, *extra]
     if verbose_ptxas:
         base += ["-Xptxas", "-v"]
     variants = [(out, tag, [f"-D{d}" for d in defines])]
-    if checks and out == LIB and not defines:
+    if checks and out == LIB and not defines and not extra:
         variants.append((LIB_CHECKS, "_checks", ["-DJT_CHECKS=1"]))
     cmds = [["g++", "-std=c++17", "-O2", "-fPIC", "-fopenmp", *inc, "-c", os.path.join(CSRC, "plan.cpp"), "-o", plan_o]]
     objs = {}
