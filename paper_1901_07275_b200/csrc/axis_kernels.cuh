@@ -1947,7 +1947,24 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
           }
         }
       }
-      if constexpr (C::VST) {  // reduce over the line's threads: shuffles in the warp, per-warp slots after
+      if constexpr (C::VST && JT_PAIRRED && LG < 32 && 2 * LG < 32) {
+        // reduce the two degrees' partials over the line's threads of the warp as a pair: the first shuffle level
+        // trades halves (lanes with the LG bit keep degree kb + 1, the others kb), so each further level moves one
+        // double instead of two (6 shuffles per term instead of 12); then per-warp slots as below
+        static_assert(C::KPT == 2, "paired reduction");
+        if (kb < k0) {
+          const int lane = threadIdx.x & 31;
+          const bool hi = (lane & LG) != 0;
+          double p = (hi ? pv[1] : pv[0]) + __shfl_xor_sync(0xffffffffu, hi ? pv[0] : pv[1], LG);
+#pragma unroll
+          for (int off = 2 * LG; off < 32; off *= 2) p += __shfl_xor_sync(0xffffffffu, p, off);
+          const int kk = hi ? 1 : 0;
+          if (lane < 2 * LG && kb + kk < k0) {
+            if constexpr (C::GW == 1) cx.alow[(kb + kk) * LG + line] = p;
+            else cx.vred[((kb + kk) * C::GW + (cx.gt >> 5)) * LG + line] = p;
+          }
+        }
+      } else if constexpr (C::VST) {  // reduce over the line's threads: shuffles in the warp, per-warp slots after
 #pragma unroll
         for (int kk = 0; kk < C::KPT; ++kk) {
           if (kb + kk < k0) {

@@ -39,6 +39,11 @@
 #ifndef JT_A1_FOLD_NMIN
 #define JT_A1_FOLD_NMIN 2048  // ... for N >= this (4096^2 forward -2.6 %; 512^3 +0.75 %, 1024 +1.2 %)
 #endif
+#ifndef JT_PAIRRED
+#define JT_PAIRRED 0  // inverse (N <= 512): the two staged degrees' (W V)^T y partials reduced over the warp as a pair
+                      // (6 shuffles per term instead of 12; measured slower, r02zx: 512^3 inverse 17.73 -> 17.89 ms,
+                      // 256^3 2.00 -> 2.03 ms, 128^3 -0.8 %)
+#endif
 #ifndef JT_ZFIRST
 #define JT_ZFIRST 1  // inverse: the first DFT layer skips the thread's zero inputs above R/2 (empty bins > N/2)
 #endif
