@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+T=r02zy
+# re-entry check of the rebuilt HEAD library: GPU suite, smoke, default bench
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_$T.txt 2>&1; echo "exit $?" >> gpurun_out/gputest_$T.txt
+tail -3 gpurun_out/gputest_$T.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$T.txt 2>&1
+tail -2 gpurun_out/smoke_$T.txt
+timeout 900 python bench.py > gpurun_out/bench_$T.json 2> gpurun_out/bench_$T.err
+tail -c 1500 gpurun_out/bench_$T.json
