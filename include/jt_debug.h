@@ -18,6 +18,20 @@ extern "C" {
 jt_status jt_debug_modified_pq(double a, double b, int64_t nt, const double *t, int kmax, double *p_out,
                                double *q_out);
 
+/* jt_debug_pair_factors: the plan's SECOND factor set of axis `axis`, used by its forward passes where the axis has
+ * one (uniform axes of FFT length 512; DESIGN.md §6 "Two real rank terms per FFT"; the method is eq:oneJ,
+ * PAPER.md:610, with a factorisation of eq:approxA whose v'_l are REAL, so two terms share one complex FFT):
+ *   *r      number of FFTs (pairs) per line, 0 if the axis has no paired set (then nothing else is written)
+ *   *rreal  number of real rank terms (2 r or 2 r - 1)
+ *   u       n x 2r complex (row-major, interleaved re/im): column 2q = P_q, 2q + 1 = conj(Q_q)
+ *   v       r x N complex: (v'_{2q} + i v'_{2q+1})[k] e^{i pi k / N} (zero for k < k0 and k >= n)
+ *   phiv    n x k0 (as jt_plan_factors), bins n int32: m_j = floor(t_j N / 2 pi) (the half-integer grid m + 1/2)
+ * so that  y_j = (phiv a_V)_j + Re sum_q ( P_q[j] Z_q[m_j] + conj(Q_q)[j] Z_q[N - 1 - m_j] ),
+ * Z_q[m] = sum_k v_q[k] a_k e^{+2 pi i k m / N}.  Host arrays owned by the caller (any may be NULL); sizes from
+ * jt_plan_info (n, N, k0) and a first call with NULL arrays (*r).  JT_ERR_ARG on a bad plan / axis. */
+jt_status jt_debug_pair_factors(jt_plan_t p, int axis, int *r, int *rreal, double *u_host, double *v_host,
+                                double *phiv_host, int32_t *bins_host);
+
 /* Virtual ranks on one GPU (tests of the distributed schedule, with only one GPU at hand).
  *
  * jt_debug_vgroup_create makes a group of `nranks` virtual ranks; jt_debug_plan_virtual then builds rank `rank`'s

@@ -38,7 +38,7 @@ EXPORTED = ["jt_default_opts", "jt_plan", "jt_plan_ex", "jt_adjoint", "jt_plan_k
             "jt_plan_nodes", "jt_plan_factors", "jt_plan_sigma", "jt_last_launches", "jt_last_error", "jt_version",
             "jt_plan_dist_ex", "jt_sync", "jt_profile", "jt_last_profile", "jt_dist_mode",
             "jt_debug_modified_pq", "jt_debug_checks", "jt_debug_vgroup_create", "jt_debug_vgroup_destroy",
-            "jt_debug_plan_virtual", "jt_debug_axis_pass_lim"]
+            "jt_debug_plan_virtual", "jt_debug_axis_pass_lim", "jt_debug_pair_factors"]
 
 JT_DIST_LOWMEM = 1
 JT_DIST_NCCL_A2A = 2  # the NCCL all-to-all instead of the fused (peer-store) exchange
@@ -437,6 +437,27 @@ def jt_plan_sigma(plan: int, axis: int):
     s = np.zeros(cnt.value)
     _check(_lib.jt_plan_sigma(plan, axis, s.ctypes.data, ctypes.byref(cnt), ctypes.byref(rmax)), "jt_plan_sigma")
     return s, rmax.value
+
+
+def jt_debug_pair_factors(plan: int, axis: int):
+    """The paired-real-term factor set of the forward passes (include/jt_debug.h): None if the axis has none, else
+    (u (n x 2r complex: P, conj(Q) per pair), v (r x N complex), phiv (n x k0), bins (n int32), rreal)."""
+    r, rr = ctypes.c_int(), ctypes.c_int()
+    _lib.jt_debug_pair_factors.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    _check(_lib.jt_debug_pair_factors(plan, axis, ctypes.byref(r), ctypes.byref(rr), None, None, None, None),
+           "jt_debug_pair_factors")
+    if r.value == 0:
+        return None
+    info = jt_plan_info(plan, axis)
+    n, N, k0 = info["n"], info["N"], info["k0"]
+    u = np.zeros((n, 2 * r.value), dtype=np.complex128)
+    v = np.zeros((r.value, N), dtype=np.complex128)
+    phiv = np.zeros((n, k0), dtype=np.float64)
+    bins = np.zeros(n, dtype=np.int32)
+    _check(_lib.jt_debug_pair_factors(plan, axis, ctypes.byref(r), ctypes.byref(rr), u.ctypes.data, v.ctypes.data,
+                                      phiv.ctypes.data, bins.ctypes.data), "jt_debug_pair_factors")
+    return u, v, phiv, bins, rr.value
 
 
 def jt_debug_modified_pq(a: float, b: float, t, kmax: int):

@@ -247,10 +247,19 @@ struct TwPrefix<N, R, NS, N> {
   static constexpr int value = 0;
 };
 
-template <int N_, int R_, int MAXR_, bool INV_, bool WG_ = false>
+template <int N_, int R_, int MAXR_, bool INV_, bool WG_ = false, bool PAIR_ = false>
 struct Cfg {
   static constexpr int N = N_, R = R_, MAXR = MAXR_;
   static constexpr bool INV = INV_;
+  // PAIR (forward only): two REAL rank terms per complex FFT.  The plan's paired factor set (jt_internal.h
+  // AxisHost::pair) has real v'_l, so X_l = F_N(v'_l (.) a) is conjugate-symmetric and the terms (l, l') share the FFT
+  // Z = F_N((v'_l + i v'_l') e^{i pi k / N} (.) a) on the half-integer bin grid m + 1/2:
+  //   Re(u_l X_l[m] + u_l' X_l'[m]) = Re(P Z[m]) + Re(conj(Q) Z[N - 1 - m]),  P = (u_l - i u_l') / 2, Q = (u_l + i u_l') / 2.
+  // A1 and the FFT are unchanged (the "v" of a pair is complex); the last pass's butterflies are dealt so that a thread
+  // owns bin m and its mirror N - 1 - m (last_v), nothing of the last butterflies is pruned, and A3 reads two factor
+  // rows (P, conj(Q)) per node: UROWS = 2 MAXR rows per bin in u~.  Bins are 0 .. N/2 - 1 (no Nyquist slot).
+  static constexpr bool PAIR = PAIR_;
+  static constexpr int UROWS = PAIR_ ? 2 * MAXR_ : MAXR_;
   // WG: one warp per group (LG = 32 / TPL lines) -- only for the term-split launches of few lines, which are
   // latency-bound (no named barriers: 256^2 0.041 -> 0.033 ms); the large launches keep 4 lines per group,
   // whose factor loads serve twice the lines per wavefront (one-warp groups measured +15 % at 512^3)
@@ -309,7 +318,7 @@ struct Cfg {
   static constexpr bool VST = N <= 512;
   static constexpr int VUN = VST ? 1 : JT_VUNROLL;  // unroll of the batch-start W V loops
   static constexpr int KPT = VST ? VST_KPT : 0;
-  static constexpr int V_BYTES = N * 16, U_BYTES = MAXR * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
+  static constexpr int V_BYTES = N * 16, U_BYTES = UROWS * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
   static constexpr int SV_BYTES = STAGED ? V_BYTES : 0;  // v_l bytes in a ring stage (URING stages hold u~_l only)
   static constexpr int STAGE_BYTES =
       SUB ? SUBB
@@ -387,6 +396,9 @@ struct Cfg {
     else return (pos + pos / R) * LG + line;
   }
   static_assert(GT % 32 == 0, "group must be whole warps");
+  static_assert(!PAIR || (!INV && MAXR == 2 && STAGED && Pass<N, R, NSL>::B % 2 == 0 && Pass<N, R, NSL>::B * TPL == N / RSL &&
+                          NSL > 1 && !VTM_PRE),
+                "PAIR: forward, staged factors, an even number of last-pass butterflies per thread");
   static_assert(RSL >= 2, "last pass radix");
   static_assert(smem_bytes() <= SMEM_LIMIT, "shared memory");
   // TMEM: 512 columns; the NT/32 warps share the 4 lane quadrants, each warp a column slice of TCOLS
@@ -505,7 +517,7 @@ struct Ring {
     }
     mbar_arrive_expect_tx(&full[s], C::SV_BYTES + C::U_BYTES + ph_bytes);
     if constexpr (C::STAGED) tma_load_1d(v(seq), gv + (long long)l * C::N, C::V_BYTES, &full[s]);
-    tma_load_1d(u(seq), gu + (long long)l * C::MAXR * C::NBINS, C::U_BYTES, &full[s]);
+    tma_load_1d(u(seq), gu + (long long)l * C::UROWS * C::NBINS, C::U_BYTES, &full[s]);
     if (kc)
       tma_load_1d(const_cast<double *>(ph(seq)), gph + (long long)l * C::KPT * C::MAXR * C::NBINS, ph_bytes, &full[s]);
   }
@@ -602,6 +614,20 @@ struct Ring {
 
 // ---- Stockham passes over the group's exchange buffer -------------------------------------------------
 
+// Butterfly index (0 .. N/RS - 1) of a thread's i-th butterfly in the pass at sub-size NS: vt + i TPL, except in
+// the LAST pass of the PAIR kernels, where butterflies 2h and 2h + 1 are v and its mirror N/RS - 1 - v, so that the
+// thread's outputs v + s N/RS and (N/RS - 1 - v) + (RS - 1 - s) N/RS = N - 1 - (v + s N/RS) are a conjugate-mirror pair.
+template <class C, int NS>
+__device__ __forceinline__ int pass_v(int vt, int i) {
+  using P = Pass<C::N, C::R, NS>;
+  if constexpr (C::PAIR && P::LAST) {
+    const int v = vt + (i / 2) * C::TPL;
+    return (i & 1) ? C::N / P::RS - 1 - v : v;
+  } else {
+    return vt + i * C::TPL;
+  }
+}
+
 // Store one real plane (SPLITX) or both (interleaved double2) of the outputs of the pass at sub-size NS.
 template <class C, int NS>
 __device__ __forceinline__ void pass_store(const double (&xr)[C::R], const double (&xi)[C::R], void *buf, int vt,
@@ -632,7 +658,7 @@ __device__ __forceinline__ void pass_load(double (&xr)[C::R], double (&xi)[C::R]
   constexpr int RS = P::RS;
 #pragma unroll
   for (int i = 0; i < P::B; ++i) {
-    const int v = vt + i * C::TPL;
+    const int v = pass_v<C, NS>(vt, i);
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
       const int sl = C::sidx(v + r * (C::N / RS), line);
@@ -719,7 +745,7 @@ __device__ __forceinline__ void pass_compute(double (&xr)[C::R], double (&xi)[C:
   } else {
 #pragma unroll
     for (int i = 0; i < P::B; ++i) {
-      const int v = vt + i * C::TPL;
+      const int v = pass_v<C, NS>(vt, i);
       if constexpr (C::TWT) {
         // this thread's twiddles w^r, r = 1..RS-1, from its TMEM slice, 8 complex per tcgen05.ld pair
         constexpr int NCHK = (RS - 1 + 7) / 8;
@@ -787,7 +813,7 @@ __device__ __forceinline__ void tw_fill(double *buf, int vt, const double2 *__re
     using P = Pass<C::N, C::R, NS>;
 #pragma unroll
     for (int i = 0; i < P::B; ++i) {
-      const int v = vt + i * C::TPL;
+      const int v = pass_v<C, NS>(vt, i);
 #pragma unroll
       for (int r = 1; r < P::RS; ++r) {
         const double2 w = __ldg(&tw[TwOff<C::N, C::R, NS>::value + (r - 1) * NS + (v % NS)]);
@@ -854,7 +880,14 @@ __device__ __forceinline__ void fft(double (&xr)[C::R], double (&xi)[C::R], void
 // Frequency index of last-pass output register e = i RSL + s.
 template <class C>
 __device__ __forceinline__ int out_pos(int vt, int e) {
-  return vt + (e / C::RSL) * C::TPL + (e % C::RSL) * (C::N / C::RSL);
+  return pass_v<C, C::NSL>(vt, e / C::RSL) + (e % C::RSL) * (C::N / C::RSL);
+}
+
+// PAIR: the register holding the conjugate-mirror bin N - 1 - m of last-pass output register e = i RSL + s:
+// butterfly i ^ 1 (pass_v), output RSL - 1 - s.
+template <class C>
+__device__ __forceinline__ constexpr int mirror_reg(int e) {
+  return ((e / C::RSL) ^ 1) * C::RSL + (C::RSL - 1 - e % C::RSL);
 }
 
 // Forward: the thread's output bins q = i (RSL/2) + s (s < RSL/2) -> register e = i RSL + s; q = R/2 is the
@@ -1109,7 +1142,7 @@ struct Ctx {
   }
   __device__ __forceinline__ const double2 *ufac(long long seq, int l) const {
     if constexpr (C::STAGED || C::URING) return ring.u(seq);
-    else return gu + (long long)l * C::MAXR * C::NBINS;
+    else return gu + (long long)l * C::UROWS * C::NBINS;
   }
   __device__ __forceinline__ void acquire(long long seq) const {
     if constexpr (C::STAGED) ring.wait_full(seq);
@@ -1688,6 +1721,21 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
           const double2 uu = __ldg(&ax.ub[((long long)l * MAXR + c) * NBINS + C::N / 2]);
           y[R / 2][c] = fma(uu.x, xr[e], y[R / 2][c]);
           y[R / 2][c] = fma(-uu.y, xi[e], y[R / 2][c]);
+        }
+      } else if constexpr (C::PAIR) {
+        // A3, paired terms: row c of bin m takes Re(P Z[m]) + Re(conj(Q) Z[N - 1 - m]) (factor rows 2c, 2c + 1)
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q) {
+          const int e = fwd_reg_of_bin<C>(q), em = mirror_reg<C>(e);
+#pragma unroll
+          for (int c = 0; c < MAXR; ++c) {
+            const double2 pp = ul[(2 * c) * NBINS + m[q]];
+            const double2 qq = ul[(2 * c + 1) * NBINS + m[q]];
+            y[q][c] = fma(pp.x, xr[e], y[q][c]);
+            y[q][c] = fma(-pp.y, xi[e], y[q][c]);
+            y[q][c] = fma(qq.x, xr[em], y[q][c]);
+            y[q][c] = fma(-qq.y, xi[em], y[q][c]);
+          }
         }
       } else
 #pragma unroll

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -108,6 +109,11 @@ struct jt_plan_s {
   int device = -2;  // -2: host-only
   jt::AxisHost host[3];
   AxisDevBuf dev[3];
+  // paired real rank terms (forward kernels with Cfg::PAIR): a second factor set per axis, used by the
+  // forward passes only (the inverse / transpose keep the unpaired complex factors)
+  bool pair[3] = {false, false, false};
+  jt::AxisHost hostp[3];
+  AxisDevBuf devp[3];
   int64_t total = 0;
   // *_host entry points: two staging slots (consecutive calls alternate, so one call's input copy overlaps the
   // previous call's output copy), their copy streams and events
@@ -185,21 +191,22 @@ struct jt_vgroup_s {
 
 namespace {
 
-jtk::AxisDev axis_dev(const jt_plan_s *p, int axis) {
-  const jt::AxisHost &h = p->host[axis];
+jtk::AxisDev axis_dev(const jt_plan_s *p, int axis, bool pair = false) {
+  const jt::AxisHost &h = pair ? p->hostp[axis] : p->host[axis];
+  const AxisDevBuf &dv = pair ? p->devp[axis] : p->dev[axis];
   jtk::AxisDev ax;
   ax.n = (int)h.n;
   ax.N = (int)h.N;
   ax.k0 = h.k0;
   ax.r = h.r;
   ax.nbins = (int)(h.N / 2 + 1);
-  ax.v = p->dev[axis].v;
-  ax.ub = p->dev[axis].ub;
-  ax.phivb = p->dev[axis].phivb;
-  ax.phivc = p->dev[axis].phivc;
-  ax.bstart = p->dev[axis].bstart;
-  ax.tw = p->dev[axis].tw;
-  ax.tw_ts = p->dev[axis].tw_ts ? p->dev[axis].tw_ts : p->dev[axis].tw;
+  ax.v = dv.v;
+  ax.ub = dv.ub;
+  ax.phivb = dv.phivb;
+  ax.phivc = dv.phivc;
+  ax.bstart = dv.bstart;
+  ax.tw = dv.tw;
+  ax.tw_ts = dv.tw_ts ? dv.tw_ts : dv.tw;
   return ax;
 }
 
@@ -213,8 +220,9 @@ jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *
                       long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
                       long long nlines_only = -1, bool allow_ts = true, long long ostride = -1,
                       long long in_lim = -1, long long out_lim = -1, bool peer = false, long long peer_row = 0) {
-  jtk::AxisDev ax = axis_dev(p, axis);
-  const int maxr = p->dev[axis].maxr;
+  const bool pr = !inverse && p->pair[axis];  // paired real terms: forward passes only
+  jtk::AxisDev ax = axis_dev(p, axis, pr);
+  const int maxr = pr ? -2 : p->dev[axis].maxr;  // (-2: launch_n's tag for the Cfg::PAIR kernels)
   // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
   const long long nlines = nlines_only >= 0 ? nlines_only : outer * inner;
   const long long ost = ostride >= 0 ? ostride : outer;
@@ -257,16 +265,17 @@ jt_status upload(T **dst, const T *src, size_t count) {
 void free_device(jt_plan_s *p) {
   if (p->device < 0) return;
   DeviceGuard g(p->device);
-  for (int i = 0; i < 3; ++i) {
-    cudaFree(p->dev[i].ub);
-    cudaFree(p->dev[i].v);
-    cudaFree(p->dev[i].tw);
-    cudaFree(p->dev[i].tw_ts);
-    cudaFree(p->dev[i].phivb);
-    cudaFree(p->dev[i].phivc);
-    cudaFree(p->dev[i].bstart);
-    p->dev[i] = AxisDevBuf();
-  }
+  for (int i = 0; i < 3; ++i)
+    for (AxisDevBuf *dv : {&p->dev[i], &p->devp[i]}) {
+      cudaFree(dv->ub);
+      cudaFree(dv->v);
+      cudaFree(dv->tw);
+      cudaFree(dv->tw_ts);
+      cudaFree(dv->phivb);
+      cudaFree(dv->phivc);
+      cudaFree(dv->bstart);
+      *dv = AxisDevBuf();
+    }
   for (int k = 0; k < JT_HOST_SLOTS; ++k) {
     cudaFree(p->stage_in[k]);
     cudaFree(p->stage_out[k]);
@@ -306,8 +315,9 @@ void free_device(jt_plan_s *p) {
   if (p->s_d2h) cudaStreamDestroy(p->s_d2h), p->s_d2h = nullptr;
 }
 
-jt_status upload_axis(jt_plan_s *p, int axis) {
-  const jt::AxisHost &h = p->host[axis];
+jt_status upload_axis(jt_plan_s *p, int axis, bool pair = false) {
+  const jt::AxisHost &h = pair ? p->hostp[axis] : p->host[axis];
+  AxisDevBuf &dv = pair ? p->devp[axis] : p->dev[axis];
   const int64_t N = h.N;
   const int r = h.r, k0 = h.k0;
   const int64_t nbins = N / 2 + 1;
@@ -317,8 +327,10 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   for (int64_t m = 0; m < nbins; ++m) maxr = std::max(maxr, h.bstart[m + 1] - h.bstart[m]);
   if (maxr > 4) return fail(JT_ERR_NUMERIC, "more than 4 nodes share one FFT bin");
   const int MAXR = maxr <= 2 ? 2 : maxr;  // 2 (Gauss-Jacobi nodes), 3 or 4 (clustered nonuniform points)
-  p->dev[axis].maxr = MAXR;
-  std::vector<double2> ub((size_t)r * nbins * MAXR, make_double2(0.0, 0.0)), v((size_t)r * N), tw(N);
+  if (pair && MAXR != 2) return fail(JT_ERR_NUMERIC, "pair: more than 2 nodes share one FFT bin");
+  dv.maxr = MAXR;
+  const int UC = pair ? 2 : 1;  // factor columns per term in h.u (pair: P and conj(Q)), rows per bin slot in ub
+  std::vector<double2> ub((size_t)r * nbins * MAXR * UC, make_double2(0.0, 0.0)), v((size_t)r * N), tw(N);
   std::vector<double> phivb((size_t)std::max(k0, 1) * nbins * MAXR, 0.0);
   constexpr int KPT = jtk::VST_KPT;  // chunk size of the kernels' staged W V (degrees per rank term)
   const int nchunk = std::max((k0 + KPT - 1) / KPT, 1);
@@ -326,10 +338,11 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   for (int64_t m = 0; m < nbins; ++m) {
     for (int c = 0; c < h.bstart[m + 1] - h.bstart[m]; ++c) {
       const int64_t j = h.bstart[m] + c;
-      for (int l = 0; l < r; ++l) {
-        const jt::cd z = h.u[(size_t)j * r + l];
-        ub[((size_t)l * MAXR + c) * nbins + m] = make_double2(z.real(), z.imag());
-      }
+      for (int l = 0; l < r; ++l)
+        for (int hh = 0; hh < UC; ++hh) {  // (pair: row 2 c of term l = P, row 2 c + 1 = conj(Q))
+          const jt::cd z = h.u[(size_t)j * r * UC + l * UC + hh];
+          ub[((size_t)l * MAXR * UC + c * UC + hh) * nbins + m] = make_double2(z.real(), z.imag());
+        }
       for (int k = 0; k < k0; ++k) {
         phivb[((size_t)k * MAXR + c) * nbins + m] = h.phiv[(size_t)j * k0 + k];
         phivc[(((size_t)(k / KPT) * nbins + m) * MAXR + c) * KPT + (k % KPT)] = h.phiv[(size_t)j * k0 + k];
@@ -362,16 +375,16 @@ jt_status upload_axis(jt_plan_s *p, int axis) {
   };
   tw = tw_table(radix_of(N, MAXR));
   jt_status s;
-  if ((s = upload(&p->dev[axis].ub, ub.data(), ub.size())) != JT_OK) return s;
-  if ((s = upload(&p->dev[axis].v, v.data(), v.size())) != JT_OK) return s;
-  if ((s = upload(&p->dev[axis].tw, tw.data(), tw.size())) != JT_OK) return s;
+  if ((s = upload(&dv.ub, ub.data(), ub.size())) != JT_OK) return s;
+  if ((s = upload(&dv.v, v.data(), v.size())) != JT_OK) return s;
+  if ((s = upload(&dv.tw, tw.data(), tw.size())) != JT_OK) return s;
   if (radix_ts_of(N, MAXR) != radix_of(N, MAXR)) {
     const std::vector<double2> tts = tw_table(radix_ts_of(N, MAXR));
-    if ((s = upload(&p->dev[axis].tw_ts, tts.data(), tts.size())) != JT_OK) return s;
+    if ((s = upload(&dv.tw_ts, tts.data(), tts.size())) != JT_OK) return s;
   }
-  if ((s = upload(&p->dev[axis].phivb, phivb.data(), phivb.size())) != JT_OK) return s;
-  if ((s = upload(&p->dev[axis].phivc, phivc.data(), phivc.size())) != JT_OK) return s;
-  if ((s = upload(&p->dev[axis].bstart, h.bstart.data(), h.bstart.size())) != JT_OK) return s;
+  if ((s = upload(&dv.phivb, phivb.data(), phivb.size())) != JT_OK) return s;
+  if ((s = upload(&dv.phivc, phivc.data(), phivc.size())) != JT_OK) return s;
+  if ((s = upload(&dv.bstart, h.bstart.data(), h.bstart.size())) != JT_OK) return s;
   return JT_OK;
 }
 
@@ -1097,6 +1110,33 @@ jt_status jt_plan_ex(jt_plan_t *out, int d, const int64_t n[], const double a[],
         return fail(s, "axis " + std::to_string(i) + ": " + err);
       }
     }
+    // Paired real rank terms for the forward passes: uniform axes whose FFT length has Cfg::PAIR
+    // kernels; the same k0; kept when it needs fewer FFTs than the complex factorisation (JT_PAIR=0 in the
+    // environment turns it off: A/B runs and tests of the unpaired forward kernels)
+    const char *pe = std::getenv("JT_PAIR");
+    const bool pair_on = JT_PAIR && !(pe && pe[0] == '0');
+    for (int i = 0; i < d && pair_on; ++i) {
+      const jt::AxisHost &h = p->host[i];
+      if (!h.uniform || !jtl::pair_length(h.N) || h.r < 2) continue;
+      int same = -1;
+      for (int k = 0; k < i; ++k)
+        if (p->pair[k] && n[k] == n[i] && a[k] == a[i] && b[k] == b[i] && p->host[k].k0 == h.k0 &&
+            p->host[k].kind == h.kind)
+          same = k;
+      if (same >= 0) {
+        p->hostp[i] = p->hostp[same];
+        p->pair[i] = true;
+        continue;
+      }
+      std::string err;
+      jt_opts oa = o;
+      oa.k0 = h.k0;
+      if (jt::build_axis_host(p->hostp[i], n[i], a[i], b[i], eps, oa, err, nullptr, h.kind, true) == JT_OK &&
+          p->hostp[i].r < h.r)
+        p->pair[i] = true;
+      else
+        p->hostp[i] = jt::AxisHost();
+    }
   } catch (const std::bad_alloc &) {
     delete p;
     return fail(JT_ERR_ALLOC, "host allocation during plan");
@@ -1114,6 +1154,7 @@ jt_status jt_plan_ex(jt_plan_t *out, int d, const int64_t n[], const double a[],
     DeviceGuard g(dev);
     for (int i = 0; i < d; ++i) {
       jt_status s = upload_axis(p, i);
+      if (s == JT_OK && p->pair[i]) s = upload_axis(p, i, true);
       if (s != JT_OK) {
         std::string msg = g_last_error;
         free_device(p);
@@ -1536,6 +1577,21 @@ jt_status jt_plan_sigma(jt_plan_t p, int axis, double *sigma, int *count, int *r
   if (count) *count = (int)h.sigma.size();
   if (rmax_used) *rmax_used = h.rmax_used;
   if (sigma) std::memcpy(sigma, h.sigma.data(), h.sigma.size() * sizeof(double));
+  return JT_OK;
+}
+
+// Test hook (declared in include/jt_debug.h): the paired-real-term factor set of the forward passes.
+jt_status jt_debug_pair_factors(jt_plan_t p, int axis, int *r, int *rreal, double *u_host, double *v_host,
+                                double *phiv_host, int32_t *bins_host) {
+  if (!p || axis < 0 || axis >= p->d) return fail(JT_ERR_ARG, "bad args");
+  const jt::AxisHost &h = p->hostp[axis];
+  if (r) *r = p->pair[axis] ? h.r : 0;
+  if (rreal) *rreal = p->pair[axis] ? h.rreal : 0;
+  if (!p->pair[axis]) return JT_OK;
+  if (u_host) std::memcpy(u_host, h.u.data(), h.u.size() * sizeof(jt::cd));
+  if (v_host) std::memcpy(v_host, h.v.data(), h.v.size() * sizeof(jt::cd));
+  if (phiv_host) std::memcpy(phiv_host, h.phiv.data(), h.phiv.size() * sizeof(double));
+  if (bins_host) std::memcpy(bins_host, h.bins.data(), h.bins.size() * sizeof(int32_t));
   return JT_OK;
 }
 

@@ -34,13 +34,20 @@ struct AxisHost {
   int rmax_used = 0;
   bool uniform = true;  // Gauss-Jacobi nodes, weighted rows (false: caller's points, unweighted)
   int kind = 0;         // 0: P~ (first kind), 1: Q~ (second kind)
+  // pair: two REAL rank terms per complex FFT (forward kernels with Cfg::PAIR).  Then bins are
+  // m_j = floor(t_j N / 2 pi) (half-integer grid m + 1/2, <= 2 rows per bin), r counts the FFTs (pairs),
+  // u is n x 2r: u[j*2r + 2q] = P_q[j], u[j*2r + 2q + 1] = conj(Q_q)[j], v[q*N + k] = (v'_{2q} + i v'_{2q+1})[k]
+  // e^{i pi k / N}, and y_j = (W V a_V)_j + Re sum_q (P_q[j] Z_q[m_j] + conj(Q_q)[j] Z_q[N - 1 - m_j]),
+  // Z_q = F_N (v_q (.) a).  rreal = the number of real terms (2r or 2r - 1).
+  bool pair = false;
+  int rreal = 0;
 };
 
 // Builds one axis's plan on the host.  Returns JT_OK or an error code with `err` filled.
 // points == nullptr: uniform (Gauss-Jacobi nodes); else n caller points in (0, pi), non-decreasing.
 // kind 0: P~, 1: Q~.
 jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double eps, const jt_opts &opts,
-                          std::string &err, const double *points = nullptr, int kind = 0);
+                          std::string &err, const double *points = nullptr, int kind = 0, bool pair = false);
 
 // Debug / test hook: P~_k(t) and Q~_k(t) (PAPER.md eq:modifiedjac, eq:modifiedjac2; reading R8 for Q~)
 // for k = 0..kmax at the angles t[0..nt-1], by the plan's own route (Cauchy transform h0 + recurrence).

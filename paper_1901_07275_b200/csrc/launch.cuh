@@ -373,9 +373,22 @@ jt_status launch_nm(LaunchState &st, bool inverse, const jtk::AxisDev &ax, const
   return launch_nmd<N, MAXR, false>(st, ax, in, out, nlines, lay, s, allow_ts);
 }
 
+// FFT lengths with Cfg::PAIR forward kernels (the last Stockham pass must hold an even number of butterflies per
+// thread, so that a thread owns bin m and its conjugate mirror N - 1 - m)
+constexpr bool pair_length(int64_t N) { return JT_PAIR && N == 512; }
+
 template <int N>
 jt_status launch_n(LaunchState &st, bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out,
                    long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
+  if (maxr == -2) {  // paired real rank terms (forward only; jt_api.cu launch_axis)
+    if constexpr (pair_length(N)) {
+      using CP = jtk::Cfg<N, radix_for<N, 2>(), 2, false, false, true>;
+      if (inverse) return fail(JT_ERR_ARG, "pair kernels are forward only");
+      return launch_cfg<CP>(st, ax, in, out, nlines, lay, s, allow_ts);
+    } else {
+      return fail(JT_ERR_ARG, "no pair kernels for this FFT length");
+    }
+  }
   if (maxr <= 2) return launch_nm<N, 2>(st, inverse, ax, in, out, nlines, lay, s, allow_ts);
   if (maxr == 3) return launch_nm<N, 3>(st, inverse, ax, in, out, nlines, lay, s, allow_ts);
   return launch_nm<N, 4>(st, inverse, ax, in, out, nlines, lay, s, allow_ts);

@@ -572,8 +572,9 @@ static void algorithm1(const ZView &Z, int r, int q, int sweeps, std::mt19937_64
 }
 
 jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double eps, const jt_opts &opts,
-                          std::string &err, const double *points, int kind) {
+                          std::string &err, const double *points, int kind, bool pair) {
   ax = AxisHost();
+  ax.pair = pair;
   ax.n = n;
   ax.N = fft_length(n);
   ax.a = a;
@@ -625,6 +626,22 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
   // (bins stay non-decreasing, rows of a bin contiguous), at most 2 bins right of its rounded bin, under a cap of 3
   // rows per bin (the kernels' MAXR = 3 instantiation: a quarter less row work than MAXR = 4), else 4; failing both,
   // the FFT length doubles.  Gauss-Jacobi nodes (<= 2 per bin) are never moved.
+  if (pair) {
+    // Paired real terms (DESIGN.md §6 "Two real rank terms per FFT"): half-integer bins m_j + 1/2 = t_j N / 2 pi
+    // rounded to the nearest half-integer, i.e. m_j = floor(t_j N / 2 pi) in [0, N/2), so that bin m and its
+    // conjugate mirror N - 1 - m pair up uniformly; at most 2 rows per bin (no spreading: the caller falls back)
+    ax.bins.assign(n, 0);
+    ax.bstart.assign(ax.N / 2 + 2, 0);
+    for (int64_t j = 0; j < n; ++j) {
+      const int32_t m = (int32_t)floorl(t[j] * (ld)ax.N / (2 * PI_L));
+      if (m < 0 || m >= ax.N / 2 || (j > 0 && m < ax.bins[j - 1]) || ax.bstart[m + 1] >= 2) {
+        err = "pair: more than 2 nodes in a half-integer FFT bin";
+        return JT_ERR_NUMERIC;
+      }
+      ax.bins[j] = m;
+      ax.bstart[m + 1]++;
+    }
+  } else
   for (;;) {
     bool ok = false;
     for (int cap : {3, 4}) {
@@ -656,8 +673,10 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
 
   // Entries: phiv (k < k0) and Z = W B (k >= k0), row by row in long double.
   const int nc = (int)(n - k0);
-  std::vector<cld> twl(N);
-  for (int64_t q = 0; q < N; ++q) twl[q] = cld(cosl(2 * PI_L * q / N), -sinl(2 * PI_L * q / N));
+  // (pair: e^{-2 pi i (m_j + 1/2) k / N} = e^{-2 pi i ((2 m_j + 1) k mod 2N) / 2N})
+  const int64_t NT = pair ? 2 * N : N;
+  std::vector<cld> twl(NT);
+  for (int64_t q = 0; q < NT; ++q) twl[q] = cld(cosl(2 * PI_L * q / NT), -sinl(2 * PI_L * q / NT));
   ax.phiv.assign((size_t)n * k0, 0.0);
   std::vector<cd> Z((size_t)n * std::max(nc, 0));
 #pragma omp parallel for schedule(dynamic, 4)
@@ -674,7 +693,7 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
         ax.phiv[(size_t)j * k0 + k] = (double)(sl * zr);
       } else {
         cld z(sl * zr, sl * zi);
-        z *= twl[(mj * k) % N];  // e^{-2 pi i m_j k / N}
+        z *= pair ? twl[((2 * mj + 1) * k) % NT] : twl[(mj * k) % N];  // e^{-2 pi i m_j k / N}
         Z[(size_t)j * nc + (k - k0)] = cd((double)z.real(), (double)z.imag());
       }
     });
@@ -722,6 +741,61 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
     double sq = std::sqrt(sig[l]);
     for (int64_t j = 0; j < n; ++j) ax.u[(size_t)j * r + l] = U0(j, l) * sq;
     for (int c = 0; c < nc; ++c) ax.v[(size_t)l * N + k0 + c] = V0h(l, c) * sq;
+  }
+  if (pair) {
+    // Two real rank terms per FFT.  Z ~ U0 diag(sig) V0h (complex rank r); the real row space of [Re Z; Im Z] has
+    // dimension r' in [r, 2r] (measured r' <= r + 1 for the Jacobi kernels): with T = diag(sig) V0h (U0 has
+    // orthonormal columns, so [Re Z; Im Z] and M = [Re T; Im T] have the same singular values and right singular
+    // vectors), the right singular vectors V' (real, orthonormal) of M above eps sigma_0 span it, and Z ~ (Z V') V'^T
+    // with REAL v'_l.  For real x = v'_l (.) alpha the FFT is conjugate-symmetric, so two terms (l, l') share one
+    // complex FFT of (v'_l + i v'_l') e^{i pi k / N} (.) alpha (half-integer bins): with P = (u_l - i u_l') / 2 and
+    // Q = (u_l + i u_l') / 2,  Re(u_l X_l[m] + u_l' X_l'[m]) = Re(P Z[m]) + Re(conj(Q) Z[N - 1 - m]).
+    int r2 = 0;
+    while (r2 < (int)sig.size() && sig[r2] > 0.01 * eps * s0) ++r2;
+    CMat Mt(nc, 2 * r2);
+    for (int l = 0; l < r2; ++l)
+      for (int c = 0; c < nc; ++c) {
+        const cd tv = V0h(l, c) * sig[l];
+        Mt(c, l) = tv.real();
+        Mt(c, r2 + l) = tv.imag();
+      }
+    CMat Us, Vs;
+    std::vector<double> ss;
+    jacobi_svd(Mt, Us, ss, Vs);
+    int rp = 0;
+    while (rp < (int)ss.size() && ss[rp] > eps * ss[0]) ++rp;
+    const int np = (rp + 1) / 2;
+    // u'_l = Z v'_l (complex), balanced like the unpaired factors: u' / sqrt(s), v' sqrt(s)
+    std::vector<cd> up((size_t)n * 2 * np, cd(0, 0));
+    std::vector<double> vp((size_t)2 * np * nc, 0.0);
+    for (int l = 0; l < rp; ++l) {
+      const double sq = std::sqrt(ss[l]);
+      for (int c = 0; c < nc; ++c) vp[(size_t)l * nc + c] = Us(c, l).real() * sq;
+#pragma omp parallel for
+      for (int64_t j = 0; j < n; ++j) {
+        cd acc(0, 0);
+        for (int c = 0; c < nc; ++c) acc += Z[(size_t)j * nc + c] * Us(c, l).real();
+        up[(size_t)j * 2 * np + l] = acc / sq;
+      }
+    }
+    ax.r = np;
+    ax.rreal = rp;
+    ax.u.assign((size_t)n * 2 * np, cd(0, 0));
+    ax.v.assign((size_t)np * N, cd(0, 0));
+    for (int q = 0; q < np; ++q) {
+      for (int64_t j = 0; j < n; ++j) {
+        const cd ua = up[(size_t)j * 2 * np + 2 * q], ub = up[(size_t)j * 2 * np + 2 * q + 1];
+        ax.u[(size_t)j * 2 * np + 2 * q] = 0.5 * (ua - cd(0, 1) * ub);                 // P
+        ax.u[(size_t)j * 2 * np + 2 * q + 1] = std::conj(0.5 * (ua + cd(0, 1) * ub));  // conj(Q)
+      }
+      for (int c = 0; c < nc; ++c) {
+        const int64_t k = k0 + c;
+        const cld ph(cosl(PI_L * k / N), sinl(PI_L * k / N));
+        const cld z = cld(vp[(size_t)(2 * q) * nc + c], vp[(size_t)(2 * q + 1) * nc + c]) * ph;
+        ax.v[(size_t)q * N + k] = cd((double)z.real(), (double)z.imag());
+      }
+    }
+    return JT_OK;
   }
   return JT_OK;
 }

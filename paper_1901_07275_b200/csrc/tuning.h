@@ -44,6 +44,11 @@
                       // (6 shuffles per term instead of 12; measured slower, r02zx: 512^3 inverse 17.73 -> 17.89 ms,
                       // 256^3 2.00 -> 2.03 ms, 128^3 -0.8 %)
 #endif
+#ifndef JT_PAIR
+#define JT_PAIR 1  // forward passes: two REAL rank terms per complex FFT (Cfg::PAIR kernels, N = 512; the plan's
+                   // second, real-row-space factor set: 9 FFTs instead of 16 per line at 512^3).  JT_PAIR=0 in the
+                   // environment turns it off at plan time (A/B)
+#endif
 #ifndef JT_ZFIRST
 #define JT_ZFIRST 1  // inverse: the first DFT layer skips the thread's zero inputs above R/2 (empty bins > N/2)
 #endif

@@ -13,6 +13,7 @@ import pytest
 
 import oracle
 import paper_1901_07275_b200 as jt
+import seeded_inputs as si
 
 CFG_PAIRS = [(0.25, -0.3), (0.1, -0.4), (-0.25, 0.35), (0.45, -0.45), (0.0, 0.0), (0.2, -0.2), (-0.4, 0.3),
              (0.35, 0.1), (0.25, -0.25)]
@@ -259,3 +260,62 @@ def test_auto_k0():
         rn = jt.Plan(n, 0.45, -0.45, 1e-12, device=-2, k0=kn).rank()
         assert p.info()["k0"] == (kn if rn <= r27 else 27) and p.rank() == min(r27, rn)
     assert jt.Plan(512, 0.25, -0.25, 1e-12, device=-2, k0=20).info()["k0"] == 20
+
+
+def pair_apply_np(plan, alpha, axis=0):
+    """The paired forward (include/jt_debug.h jt_debug_pair_factors): y = phiv a_V + Re sum_q (P_q (.) Z_q[m] +
+    conj(Q_q) (.) Z_q[N - 1 - m]), Z_q = F_N (v_q (.) a) with numpy's FFT (test-only code; the product path runs it
+    in the Cfg::PAIR kernels)."""
+    u, v, phiv, bins, rreal = jt.jt_debug_pair_factors(plan.handle, axis)
+    n, k0 = phiv.shape
+    N = v.shape[1]
+    y = phiv @ alpha[:k0]
+    for q in range(v.shape[0]):
+        x = np.zeros(N, complex)
+        x[:n] = v[q, :n] * alpha
+        Z = np.fft.ifft(x) * N
+        y = y + (u[:, 2 * q] * Z[bins]).real + (u[:, 2 * q + 1] * Z[N - 1 - bins]).real
+    return y
+
+
+@pytest.mark.parametrize("a,b", [(0.25, -0.25), (0.1, -0.4), (-0.45, 0.45), (0.0, 0.0)])
+def test_paired_factors_vs_oracle(a, b):
+    """Two real rank terms per FFT (eq:oneJ, with real v'_l): the plan's second factor set
+    of an N = 512 axis reproduces the oracle's matrix-vector product to the plan's eps with about half the FFTs, its v
+    is a real vector times e^{i pi k / N} pairwise, and its bins are the half-integer grid (2 nodes per bin)."""
+    n = 512
+    p = jt.Plan(n, a, b, 1e-12, device=-2)
+    got = jt.jt_debug_pair_factors(p.handle, 0)
+    assert got is not None
+    u, v, phiv, bins, rreal = got
+    r = p.rank()
+    assert v.shape[0] == (rreal + 1) // 2 and r <= rreal <= r + 2 and v.shape[0] < r
+    t, _ = p.nodes()
+    assert np.array_equal(bins, np.floor(t * n / (2 * np.pi)).astype(np.int32))
+    assert np.bincount(bins, minlength=n // 2).max() <= 2 and bins.max() < n // 2
+    k = np.arange(n)
+    vr = v * np.exp(-1j * np.pi * k / n)  # (v'_{2q} + i v'_{2q+1}): both parts real vectors, zero below k0
+    k0 = p.info()["k0"]
+    assert np.all(vr[:, :k0] == 0)
+    x = si.gaussian((n,), seed=5)
+    ref = oracle.phi(n, a, b) @ x
+    y = pair_apply_np(p, x)
+    assert np.linalg.norm(y - ref) <= 1e-11 * np.linalg.norm(ref)
+    # the unit vectors of a few degrees: column by column against the oracle's matrix
+    Phi = oracle.phi(n, a, b)
+    for kk in (0, k0 - 1, k0, k0 + 1, 100, n - 1):
+        e = np.zeros(n)
+        e[kk] = 1.0
+        assert np.linalg.norm(pair_apply_np(p, e) - Phi[:, kk]) <= 2e-11 * np.linalg.norm(Phi[:, kk])
+    p.close()
+
+
+def test_pair_env_off(monkeypatch):
+    monkeypatch.setenv("JT_PAIR", "0")
+    p = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2)
+    assert jt.jt_debug_pair_factors(p.handle, 0) is None
+    p.close()
+    q = jt.Plan(256, 0.25, -0.25, 1e-12, device=-2)  # no paired kernels at this FFT length
+    monkeypatch.delenv("JT_PAIR")
+    assert jt.jt_debug_pair_factors(q.handle, 0) is None
+    q.close()
