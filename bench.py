@@ -44,6 +44,20 @@ def algorithmic_flops_per_point(N: int, r: int, k0: int = K0) -> float:
     return r * (5 * np.log2(N) + 6) + 2 * k0
 
 
+def executed_flops_per_point(N: int, ffts: int, k0: int = K0) -> float:
+    """The same count for the schedule a paired axis executes (DESIGN.md §6 "Two real rank terms per FFT"): per FFT
+    5 log2 N + 2 (column scale, complex x real) + 8 (two factor rows per node: P Z[m] and conj(Q) Z[N-1-m])."""
+    return ffts * (5 * np.log2(N) + 10) + 2 * k0
+
+
+def ffts_per_line(handle, axis: int, rank: int, nlines: int) -> int:
+    """Complex FFTs per line of a forward pass of this axis: the paired factor set's pair count where the plan has
+    one and the launch has enough lines for it (csrc/tuning.h JT_PAIR_MIN_LINES), else the rank."""
+    import paper_1901_07275_b200 as jt
+    got = jt.jt_debug_pair_factors(handle, axis)
+    return int(got[1].shape[0]) if (got is not None and nlines >= 2400) else int(rank)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -367,6 +381,11 @@ def main():
         ax_dom = strides[i_dom][0]
         flops = algorithmic_flops_per_point(infos[ax_dom]["N"], ranks[ax_dom], k0s[ax_dom]) * total_points
         achieved = flops / (per_axis_ms[i_dom] * 1e-3) / 1e12
+        # what the launch executes: paired axes run ~half as many FFTs as the rank (two real terms per complex FFT)
+        nfft = [ffts_per_line(plan.handle, ax, ranks[ax], total_points // shape[ax]) for ax in range(d)]
+        flops_x = executed_flops_per_point(infos[ax_dom]["N"], nfft[ax_dom], k0s[ax_dom]) * total_points \
+            if nfft[ax_dom] != ranks[ax_dom] else flops
+        achieved_x = flops_x / (per_axis_ms[i_dom] * 1e-3) / 1e12
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -379,6 +398,11 @@ def main():
                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                     "kernel": f"fwd_axis_kernel<N={shape[ax_dom]}> (axis {ax_dom})",
                     "flops_per_launch": flops,
+                    # `achieved` / `frac` count the algorithmic work of SURVEY.md §8(d) (the paper's schedule: one
+                    # complex FFT per rank term, r = the plan's rank); `executed` counts the FFTs the launch really
+                    # runs
+                    "executed": {"ffts_per_line_per_axis": nfft, "flops_per_launch": flops_x, "achieved": achieved_x,
+                                 "frac": achieved_x / FP64_PEAK_TFLOPS},
                     "per_axis_ms_launch_order": [round(float(v), 4) for v in per_axis_ms],
                     "hbm_algorithmic_GBps": hbm_bytes / (per_axis_ms[i_dom] * 1e-3) / 1e9,
                     # ncu-measured DRAM bytes of one launch (profiles/ncu_summary.json) over the live launch time

@@ -186,6 +186,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 constexpr int K0MAX = 32;   // largest dense low-degree block (jt_opts.k0)
 constexpr int VST_KPT = 2;  // degrees of W V staged per rank term (N <= 512), read as double2 pairs
+constexpr int VST_KPT_PAIR = 4;  // ... per FFT of the PAIR kernels (half as many terms: the whole block stays in the ring)
                             // (4 measured slower: a bigger stage leaves room for only 2 ring stages)
 constexpr int SMEM_LIMIT = 227 * 1024;
 
@@ -274,6 +275,9 @@ struct Cfg {
   static constexpr int RSL = Pass<N, R, NSL>::RS;                       // ... with radix RSL
   static constexpr int NB = R / 2 + 1;                                  // bins per thread (R/2 + Nyquist slot)
   static constexpr int NBINS = N / 2 + 1;
+  // bin slots per thread in the row-range table and (inverse) the input state: the PAIR inverse also holds the rows
+  // of its first-pass MIRROR positions' bins (slots R/2 .. R-1, see inv_axis_kernel)
+  static constexpr int NBT = (PAIR_ && INV_) ? R_ : R_ / 2 + 1;
   // Register budget (32-bit registers): a thread holds x (4R), its persistent input state (the
   // coefficients a, or the inverse's input-bin values: 2R resp. 2 NB MAXR) and its output accumulators
   // (the forward's bin rows y: 2 NB MAXR, or the inverse's acc: 2R).  For R >= 32 that exceeds 255, so
@@ -295,7 +299,7 @@ struct Cfg {
   // exchange buffer: slots [pos][line], LG pad slots after every R positions -> the strided first-pass
   // stores and the unit-stride loads are both free of bank conflicts
   static constexpr int SLOTS = Pass<N, R, 1>::LAST ? 0 : (N + N / R) * LG;
-  static constexpr int PSTATE = PRIV ? (INV ? NB * MAXR : R) : 0;  // private doubles per thread (inverse: bin rows)
+  static constexpr int PSTATE = PRIV ? (INV ? NBT * MAXR : R) : 0;  // private doubles per thread (inverse: bin rows)
   static constexpr int PSLOTS = TPRIV ? 0 : PSTATE;                           // ... of them in SMEM
   // + (inverse) the per-warp partial sums of (W V)^T y (K0MAX x GW x LG)
   static constexpr int VRED = INV ? K0MAX * GW * LG : 0;
@@ -317,7 +321,7 @@ struct Cfg {
   static constexpr int SUBB = 16384, NSUB = 8;  // bytes per sub-stage, sub-stages per term
   static constexpr bool VST = N <= 512;
   static constexpr int VUN = VST ? 1 : JT_VUNROLL;  // unroll of the batch-start W V loops
-  static constexpr int KPT = VST ? VST_KPT : 0;
+  static constexpr int KPT = VST ? (PAIR ? VST_KPT_PAIR : VST_KPT) : 0;
   static constexpr int V_BYTES = N * 16, U_BYTES = UROWS * NBINS * 16, PH_BYTES = KPT * MAXR * NBINS * 8;
   static constexpr int SV_BYTES = STAGED ? V_BYTES : 0;  // v_l bytes in a ring stage (URING stages hold u~_l only)
   static constexpr int STAGE_BYTES =
@@ -348,7 +352,7 @@ struct Cfg {
   static constexpr bool TW_QSHARE = TW_SHARED || VTM;  // one twiddle copy per lane quadrant
   static constexpr int TW_BYTES = (TWS && !TWT) ? (TwTotal<N, R>::value * 16 + 127) / 128 * 128 : 0;
   // per-CTA table of the row range of every (thread position vt, bin slot q): (j0 << 4) | count
-  static constexpr int BINFO_BYTES = STAGED ? (TPL * NB * 4 + 127) / 128 * 128 : 0;
+  static constexpr int BINFO_BYTES = STAGED ? (TPL * NBT * 4 + 127) / 128 * 128 : 0;
   static constexpr int VTM_BYTES = VTM_PRE ? 16 : 0;  // (VTM: v-ready mbarrier + v-consumed counter after the ring)
   static constexpr int hdr_bytes(int nstage) {
     return (nstage * STAGE_BYTES + 3 * nstage * 8 + VTM_BYTES + 127) / 128 * 128 + BINFO_BYTES + TW_BYTES;
@@ -396,9 +400,11 @@ struct Cfg {
     else return (pos + pos / R) * LG + line;
   }
   static_assert(GT % 32 == 0, "group must be whole warps");
-  static_assert(!PAIR || (!INV && MAXR == 2 && STAGED && Pass<N, R, NSL>::B % 2 == 0 && Pass<N, R, NSL>::B * TPL == N / RSL &&
-                          NSL > 1 && !VTM_PRE),
-                "PAIR: forward, staged factors, an even number of last-pass butterflies per thread");
+  static_assert(!PAIR || INV || (MAXR == 2 && Pass<N, R, NSL>::B % 2 == 0 && Pass<N, R, NSL>::B * TPL == N / RSL &&
+                                 NSL > 1 && !VTM_PRE && !SUB && !URING_WANT),
+                "PAIR forward: an even number of last-pass butterflies per thread");
+  static_assert(!PAIR || !INV || (MAXR == 2 && Pass<N, R, 1>::B == 1 && Pass<N, R, 1>::RS == R && PRIV && !SUB),
+                "PAIR inverse: one radix-R first-pass butterfly per thread (positions vt + r TPL)");
   static_assert(RSL >= 2, "last pass radix");
   static_assert(smem_bytes() <= SMEM_LIMIT, "shared memory");
   // TMEM: 512 columns; the NT/32 warps share the 4 lane quadrants, each warp a column slice of TCOLS
@@ -620,7 +626,7 @@ struct Ring {
 template <class C, int NS>
 __device__ __forceinline__ int pass_v(int vt, int i) {
   using P = Pass<C::N, C::R, NS>;
-  if constexpr (C::PAIR && P::LAST) {
+  if constexpr (C::PAIR && !C::INV && P::LAST) {
     const int v = vt + (i / 2) * C::TPL;
     return (i & 1) ? C::N / P::RS - 1 - v : v;
   } else {
@@ -992,7 +998,7 @@ struct Ctx {
   }
   __device__ __forceinline__ void rows_of(const int *__restrict__ bstart, int q, int m, int &j0, int &cnt) const {
     if constexpr (C::STAGED) {
-      const int bi = binfo()[vt * C::NB + q];
+      const int bi = binfo()[vt * C::NBT + q];
       j0 = bi >> 4;
       cnt = bi & 15;
     } else {
@@ -1023,8 +1029,8 @@ struct Ctx {
         for (long long q = 0; q < C::NSTAGE && q < ring.total; ++q) ring.issue(q);
       }
     }
-    if constexpr (C::STAGED) for (int i = threadIdx.x; i < C::TPL * C::NB; i += C::NT) {
-      const int m = binof(i / C::NB, i % C::NB);
+    if constexpr (C::STAGED) for (int i = threadIdx.x; i < C::TPL * C::NBT; i += C::NT) {
+      const int m = binof(i / C::NBT, i % C::NBT);
       if (!JT_CHK(m >= 0 && m < C::NBINS)) continue;
       const int j0 = __ldg(&bstart[m]);
       binfo()[i] = (j0 << 4) | (__ldg(&bstart[m + 1]) - j0);
@@ -1570,18 +1576,25 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
       const double2 *vl = cx.vfac(seq, l);
       const double2 *ul = cx.ufac(seq, l);
       if constexpr (C::VST) {  // A4 for degrees l KPT .. l KPT + KPT - 1 (rows of W V staged with the term)
-        static_assert(C::KPT == 2, "W V chunks are read as double2 pairs");
+        static_assert(C::KPT % 2 == 0 && K0MAX % C::KPT == 0, "W V chunks are read as double2 pairs");
+        constexpr int KP2 = C::KPT / 2;
         const double2 *ph = reinterpret_cast<const double2 *>(cx.ring.ph(seq));
         const int kb = l * C::KPT;
-        if (kb < k0) {  // chunk layout [m][c][kk]; degree kb + 1 >= k0 is zero-padded (alow padded too)
-          const double a0 = cx.alow[kb * LG + line], a1 = cx.alow[(kb + 1) * LG + line];
+        if (kb < k0) {  // chunk layout [m][c][kk]; degrees >= k0 of the chunk are zero-padded (alow padded too)
+          double al[C::KPT];
 #pragma unroll
-          for (int q = 0; q < NB; ++q)
+          for (int kk = 0; kk < C::KPT; ++kk) al[kk] = cx.alow[(kb + kk) * LG + line];
 #pragma unroll
-            for (int c = 0; c < MAXR; ++c) {
-              const double2 pp = ph[m[q] * MAXR + c];
-              y[q][c] = fma(pp.x, a0, fma(pp.y, a1, y[q][c]));
-            }
+          for (int q = 0; q < NB; ++q) {
+            if (C::PAIR && q == R / 2) continue;  // (no Nyquist slot on the half-integer bin grid)
+#pragma unroll
+            for (int c = 0; c < MAXR; ++c)
+#pragma unroll
+              for (int hh = 0; hh < KP2; ++hh) {
+                const double2 pp = ph[(m[q] * MAXR + c) * KP2 + hh];
+                y[q][c] = fma(pp.x, al[2 * hh], fma(pp.y, al[2 * hh + 1], y[q][c]));
+              }
+          }
         }
       }
       double xr[R], xi[R];
@@ -1798,12 +1811,21 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
 template <class C, bool SPLIT, bool TSPLIT = false>
 __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, const double *in, double *out,
                                                              long long nlines, Layout lay, TermSplit ts) {
-  constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NB, MAXR = C::MAXR, NBINS = C::NBINS;
+  // PAIR (the transpose of the paired forward, Cfg::PAIR): a = (W V)^T y + Re(w (.) F_N b) with b[m] = sum of P_j y_j and
+  // b[N - 1 - m] = sum of conj(Q)_j y_j over the rows j of bin m.  A thread's first-pass positions vt + r TPL are bins
+  // for r < R/2 (slots q = r: its own rows, factor rows P) and mirrors for r >= R/2: position vt + r TPL =
+  // N - 1 - m with m = (TPL - 1 - vt) + (R - 1 - r) TPL, so slot q = R/2 + (R - 1 - r) holds the rows of THAT bin
+  // (factor rows conj(Q)); NB here = C::NBT = R slots, no Nyquist slot, no empty upper half.
+  constexpr int R = C::R, TPL = C::TPL, LG = C::LG, NB = C::NBT, MAXR = C::MAXR, NBINS = C::NBINS;
+  constexpr int NBO = C::PAIR ? R / 2 : NB;  // slots of the thread's OWN rows (the dense block sums each row once)
   extern __shared__ __align__(128) char smem_raw[];
   Phases phs;
   pdl_trigger();
   Ctx<C, TSPLIT> cx(smem_raw, ax, nlines, ts);
-  cx.start(ax.bstart, ax.tw, [](int vt_, int q) { return q < R / 2 ? vt_ + q * TPL : C::N / 2; });
+  cx.start(ax.bstart, ax.tw, [](int vt_, int q) {
+    if constexpr (C::PAIR) return q < R / 2 ? vt_ + q * TPL : (TPL - 1 - vt_) + (q - R / 2) * TPL;
+    else return q < R / 2 ? vt_ + q * TPL : C::N / 2;
+  });
   // (term split, latency-bound: the batch's input lines requested into L2 while the previous kernel finishes -- only a
   // cache hint, so it may precede the dependency wait: L2 is the point of coherence)
   if constexpr (TSPLIT && JT_PDL_PREFETCH)
@@ -1819,7 +1841,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
   // input bins: q < R/2 -> first-pass position vt + q TPL; q = R/2 -> position vt + N/2 (Nyquist, vt == 0)
   int m[NB];
 #pragma unroll
-  for (int q = 0; q < NB; ++q) m[q] = q < R / 2 ? vt + q * TPL : C::N / 2;
+  for (int q = 0; q < NB; ++q)
+    m[q] = q < R / 2 ? vt + q * TPL : (C::PAIR ? (TPL - 1 - vt) + (q - R / 2) * TPL : C::N / 2);
 
   long long seq = 0;
   for (long long bt = cx.bt0; bt < cx.nbatch; bt += cx.btstep) {
@@ -1836,7 +1859,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
       double yr[NB * MAXR];
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
-        const bool own = q < R / 2 || vt == 0;
+        const bool own = C::PAIR || q < R / 2 || vt == 0;
         int j0, cnt;
         cx.rows_of(ax.bstart, q, m[q], j0, cnt);
 #pragma unroll
@@ -1859,7 +1882,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
         const double *pk = ax.phivb + (long long)k * MAXR * NBINS;
         double p = 0.0;
 #pragma unroll
-        for (int q = 0; q < NB; ++q) {
+        for (int q = 0; q < NBO; ++q) {
           double pv[MAXR];
           load_rows<MAXR>(pk + m[q], NBINS, pv);
 #pragma unroll
@@ -1948,7 +1971,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
           xr[R / 2] = fma(uu.x, yc[c], xr[R / 2]);
           xi[R / 2] = fma(uu.y, yc[c], xi[R / 2]);
         }
-      } else if constexpr (!C::STAGED && !C::VST && MAXR == 2 && (JT_LOADS_FIRST & 2) && C::N >= JT_LF_INV_NMIN) {
+      } else if constexpr (!C::PAIR && !C::STAGED && !C::VST && MAXR == 2 && (JT_LOADS_FIRST & 2) && C::N >= JT_LF_INV_NMIN) {
         // u~_l from L1/L2: both rows' loads of every bin in flight before the state chunks
         double2 u1[NB];
 #pragma unroll
@@ -1981,15 +2004,21 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
           const int idx = ch * YS::CH + i;
           if (idx < NB * MAXR) {
             const int r = idx / MAXR, c = idx % MAXR;
-            const double2 uu = ul[c * NBINS + m[r]];
+            // (PAIR: slots >= R/2 are the mirror positions' bins: factor row conj(Q), input register R - 1 - (r - R/2))
+            const bool mir = C::PAIR && r >= R / 2;
+            const int reg = mir ? R - 1 - (r - R / 2) : r;
+            const double2 uu = ul[(C::PAIR ? 2 * c + (mir ? 1 : 0) : c) * NBINS + m[r]];
             const double yv = yc[i];
-            xr[r] = fma(uu.x, yv, xr[r]);
-            xi[r] = fma(uu.y, yv, xi[r]);
+            xr[reg] = fma(uu.x, yv, xr[reg]);
+            xi[reg] = fma(uu.y, yv, xi[reg]);
             if constexpr (C::VST) {
-              if (kb < k0) {
-                const double2 pp = ph[m[r] * MAXR + c];
-                pv[0] = fma(pp.x, yv, pv[0]);
-                pv[1] = fma(pp.y, yv, pv[1]);
+              if (!mir && kb < k0) {
+#pragma unroll
+                for (int hh = 0; hh < C::KPT / 2; ++hh) {
+                  const double2 pp = ph[(m[r] * MAXR + c) * (C::KPT / 2) + hh];
+                  pv[2 * hh] = fma(pp.x, yv, pv[2 * hh]);
+                  pv[2 * hh + 1] = fma(pp.y, yv, pv[2 * hh + 1]);
+                }
               }
             }
           }
@@ -2032,7 +2061,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
 #pragma unroll
         for (int e = 0; e < R; ++e) asm volatile("prefetch.global.L1 [%0];" ::"l"(vl + out_pos<C>(vt, e)));
       }
-      fft<C, false, true>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // (inputs above R/2: empty bins)
+      fft<C, false, !C::PAIR>(xr, xi, cx.buf, vt, line, ax.tw + (l >> 30), cx.ttw);  // (unpaired: inputs above R/2 are empty bins)
       if constexpr (C::SUB) {
         // a[k] += Re(v_l[k] B[k]) from the ring: sub-stage 4 + j holds v_l[1024 h + 256 j + ...], i.e. the outputs
         // e with e / RSL in {2j, 2j + 1} (k = vt + (e / RSL) TPL + (e % RSL) N / RSL, RSL = 4)

@@ -220,11 +220,14 @@ jt_status launch_axis(const jt_plan_s *p, int axis, bool inverse, const double *
                       long long inner, cudaStream_t s, int in_split = 1, int out_split = 1,
                       long long nlines_only = -1, bool allow_ts = true, long long ostride = -1,
                       long long in_lim = -1, long long out_lim = -1, bool peer = false, long long peer_row = 0) {
-  const bool pr = !inverse && p->pair[axis];  // paired real terms: forward passes only
-  jtk::AxisDev ax = axis_dev(p, axis, pr);
-  const int maxr = pr ? -2 : p->dev[axis].maxr;  // (-2: launch_n's tag for the Cfg::PAIR kernels)
   // nlines_only >= 0: only the first nlines_only lines (a column block of an outer == 1 pass)
   const long long nlines = nlines_only >= 0 ? nlines_only : outer * inner;
+  // paired real terms: forward passes only, and only launches with enough lines to fill the GPU without a term
+  // split (the few-line, latency-bound launches keep the unpaired kernels and their one-warp-group / cluster term
+  // split: 256^2 forward 27 us unpaired vs 35 us paired, r02zz3)
+  const bool pr = p->pair[axis] && nlines >= JT_PAIR_MIN_LINES && (!inverse || JT_PAIR_INV);
+  jtk::AxisDev ax = axis_dev(p, axis, pr);
+  const int maxr = pr ? -2 : p->dev[axis].maxr;  // (-2: launch_n's tag for the Cfg::PAIR kernels)
   const long long ost = ostride >= 0 ? ostride : outer;
   const long long n = p->n[axis];
   const long long geo_in = (in_split > 1 ? ost : outer) * n * inner, geo_out = (out_split > 1 ? ost : outer) * n * inner;
@@ -332,7 +335,7 @@ jt_status upload_axis(jt_plan_s *p, int axis, bool pair = false) {
   const int UC = pair ? 2 : 1;  // factor columns per term in h.u (pair: P and conj(Q)), rows per bin slot in ub
   std::vector<double2> ub((size_t)r * nbins * MAXR * UC, make_double2(0.0, 0.0)), v((size_t)r * N), tw(N);
   std::vector<double> phivb((size_t)std::max(k0, 1) * nbins * MAXR, 0.0);
-  constexpr int KPT = jtk::VST_KPT;  // chunk size of the kernels' staged W V (degrees per rank term)
+  const int KPT = pair ? jtk::VST_KPT_PAIR : jtk::VST_KPT;  // chunk size of the kernels' staged W V (degrees per term)
   const int nchunk = std::max((k0 + KPT - 1) / KPT, 1);
   std::vector<double> phivc((size_t)nchunk * nbins * MAXR * KPT, 0.0);
   for (int64_t m = 0; m < nbins; ++m) {
@@ -373,12 +376,12 @@ jt_status upload_axis(jt_plan_s *p, int axis, bool pair = false) {
     if (t.empty()) t.push_back(make_double2(1.0, 0.0));
     return t;
   };
-  tw = tw_table(radix_of(N, MAXR));
+  tw = tw_table(pair ? pair_radix(N) : radix_of(N, MAXR));
   jt_status s;
   if ((s = upload(&dv.ub, ub.data(), ub.size())) != JT_OK) return s;
   if ((s = upload(&dv.v, v.data(), v.size())) != JT_OK) return s;
   if ((s = upload(&dv.tw, tw.data(), tw.size())) != JT_OK) return s;
-  if (radix_ts_of(N, MAXR) != radix_of(N, MAXR)) {
+  if (!pair && radix_ts_of(N, MAXR) != radix_of(N, MAXR)) {
     const std::vector<double2> tts = tw_table(radix_ts_of(N, MAXR));
     if ((s = upload(&dv.tw_ts, tts.data(), tts.size())) != JT_OK) return s;
   }

@@ -374,16 +374,19 @@ jt_status launch_nm(LaunchState &st, bool inverse, const jtk::AxisDev &ax, const
 }
 
 // FFT lengths with Cfg::PAIR forward kernels (the last Stockham pass must hold an even number of butterflies per
-// thread, so that a thread owns bin m and its conjugate mirror N - 1 - m)
-constexpr bool pair_length(int64_t N) { return JT_PAIR && N == 512; }
+// thread, so that a thread owns bin m and its conjugate mirror N - 1 - m): 512 = 32 x 16 (2 butterflies), 4096 =
+// 32 x 32 x 4 (8), and 256 as 32 x 8 (4; the unpaired N = 256 kernels are radix 16 = 16 x 16, one butterfly)
+constexpr bool pair_length(int64_t N) { return JT_PAIR && (N == 512 || N == 256 || N == 4096); }
+constexpr int pair_radix(int64_t N) { return N == 256 ? 32 : radix_of(N, 2); }
 
 template <int N>
 jt_status launch_n(LaunchState &st, bool inverse, int maxr, const jtk::AxisDev &ax, const double *in, double *out,
                    long long nlines, const jtk::Layout &lay, cudaStream_t s, bool allow_ts) {
-  if (maxr == -2) {  // paired real rank terms (forward only; jt_api.cu launch_axis)
+  if (maxr == -2) {  // paired real rank terms (jt_api.cu launch_axis)
     if constexpr (pair_length(N)) {
-      using CP = jtk::Cfg<N, radix_for<N, 2>(), 2, false, false, true>;
-      if (inverse) return fail(JT_ERR_ARG, "pair kernels are forward only");
+      using CP = jtk::Cfg<N, pair_radix(N), 2, false, false, true>;
+      using CI = jtk::Cfg<N, pair_radix(N), 2, true, false, true>;
+      if (inverse) return launch_cfg<CI>(st, ax, in, out, nlines, lay, s, allow_ts);
       return launch_cfg<CP>(st, ax, in, out, nlines, lay, s, allow_ts);
     } else {
       return fail(JT_ERR_ARG, "no pair kernels for this FFT length");

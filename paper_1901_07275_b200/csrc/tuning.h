@@ -49,6 +49,13 @@
                    // second, real-row-space factor set: 9 FFTs instead of 16 per line at 512^3).  JT_PAIR=0 in the
                    // environment turns it off at plan time (A/B)
 #endif
+#ifndef JT_PAIR_INV
+#define JT_PAIR_INV 1  // ... also the inverse / transpose passes (the transposed paired operator)
+#endif
+#ifndef JT_PAIR_MIN_LINES
+#define JT_PAIR_MIN_LINES 2400  // ... for launches of at least this many lines (below, the term-split launches of the
+                                // unpaired kernels are faster: 256^2 forward 27 vs 35 us)
+#endif
 #ifndef JT_ZFIRST
 #define JT_ZFIRST 1  // inverse: the first DFT layer skips the thread's zero inputs above R/2 (empty bins > N/2)
 #endif

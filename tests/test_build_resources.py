@@ -29,10 +29,12 @@ def res_usage():
     return res
 
 
-@pytest.mark.parametrize("direction,inv", [("fwd", 0), ("inv", 1)])
-def test_bench_kernels_do_not_spill(direction, inv):
+@pytest.mark.parametrize("direction,inv,pair", [("fwd", 0, 1), ("fwd", 0, 0), ("inv", 1, 0)])
+def test_bench_kernels_do_not_spill(direction, inv, pair):
+    """(Cfg<N, R, MAXR, INV, WG, PAIR>: the bench's forward is the PAIR kernel; the unpaired forward stays for the
+    few-line launches and JT_PAIR=0.)"""
     res = res_usage()
-    key = f"{direction}_axis_kernelINS_3CfgILi512ELi32ELi2ELb{inv}ELb0EEELb0ELb0EE"
+    key = f"{direction}_axis_kernelINS_3CfgILi512ELi32ELi2ELb{inv}ELb0ELb{pair}EEELb0ELb0EE"
     hits = [v for k, v in res.items() if key in k]
     assert len(hits) == 1, key
     r = hits[0]

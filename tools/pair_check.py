@@ -17,7 +17,9 @@ def child():
     import seeded_inputs as si
     out = {}
     cases = [((512,), (0.25,), (-0.25,)), ((512, 24), (0.1, 0.2), (-0.4, 0.3)), ((40, 512), (0.2, 0.0), (0.3, 0.0)),
-             ((512, 512), (0.25, -0.3), (-0.25, 0.2)), ((8, 512, 512), (0.1, 0.25, -0.45), (0.2, -0.25, 0.45))]
+             ((512, 512), (0.25, -0.3), (-0.25, 0.2)), ((8, 512, 512), (0.1, 0.25, -0.45), (0.2, -0.25, 0.45)),
+             ((256,), (0.2,), (-0.2,)), ((256, 40), (-0.4, 0.1), (0.3, 0.2)), ((24, 256, 256), (0.0, 0.35, 0.1), (0.0, 0.1, -0.4)),
+             ((4096,), (0.45,), (-0.45,)), ((3, 4096), (0.1, 0.0), (0.1, 0.0)), ((4096, 5), (-0.3, 0.0), (0.3, 0.0))]
     for shape, a, b in cases:
         p = jt.Plan(shape, a, b, 1e-12)
         x = si.gaussian(shape, seed=1)
@@ -35,21 +37,53 @@ def child():
                                            "pairs": [(jt.jt_debug_pair_factors(p.handle, i) or [None, np.zeros((0, 0))])[1].shape[0]
                                                      for i in range(len(shape))]}
         p.close()
-    # timing: 512^3 forward
+    # timing: the BASELINE configs' forwards, sampled oracle check of the full-size outputs
+    for name in ("cfg2_2d_256", "cfg4_3d_256", "cfg3_2d_4096", "cfg5_3d_512"):
+        c = si.CONFIGS[name]
+        shape = tuple(c["n"])
+        p = jt.Plan(shape, c["a"], c["b"], c["eps"])
+        x = si.gaussian(shape, seed=0)
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        for _ in range(3):
+            jt.jt_forward(p.handle, xd, yd)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            jt.jt_forward(p.handle, xd, yd)
+        e1.record()
+        torch.cuda.synchronize()
+        idx = np.stack([np.random.default_rng(3).integers(0, shape[i], 32) for i in range(len(shape))], axis=1)
+        ref = oracle.forward_at(x, c["a"], c["b"], idx)
+        got = yd.cpu().numpy()[tuple(idx[:, i] for i in range(len(shape)))]
+        zd = torch.empty_like(xd)
+        for _ in range(3):
+            jt.jt_inverse(p.handle, yd, zd)
+        torch.cuda.synchronize()
+        rt = float(np.linalg.norm(zd.cpu().numpy() - x) / np.linalg.norm(x))
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record()
+        for _ in range(20):
+            jt.jt_inverse(p.handle, yd, zd)
+        i1.record()
+        torch.cuda.synchronize()
+        jt.jt_inverse(p.handle, xd, zd)  # the inverse of independent values against the oracle's inverse, sampled
+        torch.cuda.synchronize()
+        iref = oracle.inverse_at(x, c["a"], c["b"], idx)
+        igot = zd.cpu().numpy()[tuple(idx[:, i] for i in range(len(shape)))]
+        out[name] = {"fwd_ms": e0.elapsed_time(e1) / 20, "inv_ms": i0.elapsed_time(i1) / 20, "roundtrip": rt,
+                     "inv_sampled_err": float(np.linalg.norm(igot - iref) / np.linalg.norm(iref)),
+                     "sampled_err": float(np.linalg.norm(got - ref) / np.linalg.norm(ref)),
+                     "ranks": [p.rank(i) for i in range(len(shape))],
+                     "pairs": [(jt.jt_debug_pair_factors(p.handle, i) or [None, np.zeros((0, 0))])[1].shape[0] for i in range(len(shape))]}
+        p.close()
     shape = (512, 512, 512)
     p = jt.Plan(shape, (0.25,) * 3, (-0.25,) * 3, 1e-12)
     xd = torch.from_numpy(si.gaussian(shape, seed=0)).cuda()
     yd = torch.empty_like(xd)
-    for _ in range(3):
-        jt.jt_forward(p.handle, xd, yd)
+    jt.jt_forward(p.handle, xd, yd)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(10):
-        jt.jt_forward(p.handle, xd, yd)
-    e1.record()
-    torch.cuda.synchronize()
-    out["512^3_fwd_ms"] = e0.elapsed_time(e1) / 10
     # sampled oracle check of the full-size output
     idx = np.stack([np.random.default_rng(3).integers(0, 512, 64) for _ in range(3)], axis=1)
     x = si.gaussian(shape, seed=0)
