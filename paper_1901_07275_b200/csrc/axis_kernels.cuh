@@ -52,8 +52,9 @@ struct AxisDev {
   const double2 *v;      // r x N        v_l[k] at v[l N + k] (zero for k < k0 and k >= n)
   const double2 *ub;     // r x MAXR x nbins   u~_l of row bstart[m] + c at ub[(l MAXR + c) nbins + m] (0-padded)
   const double *phivb;   // k0 x MAXR x nbins  (W V)[bstart[m] + c, k] at phivb[(k MAXR + c) nbins + m] (0-padded)
-  const double *phivc;   // the same in chunks of VST_KPT degrees: (W V)[bstart[m] + c, KPT l + kk] at
-                         // phivc[((l nbins + m) MAXR + c) KPT + kk], l < ceil(k0 / KPT) (0-padded)
+  const double *phivc;   // the same in chunks of 2 degrees: (W V)[bstart[m] + c, 2 h + kk] at
+                         // phivc[((h nbins + m) MAXR + c) 2 + kk], h < ceil(k0 / KPT) KPT / 2 (0-padded); a ring stage
+                         // takes the KPT / 2 consecutive chunks of its term
   const int *bstart;     // nbins + 1 row offsets: rows of bin m are bstart[m] .. bstart[m+1]-1
   const double2 *tw;     // per-pass twiddle tables, see TwOff (pass NS, radix RS: (RS-1) NS entries,
                          // entry (r-1) NS + j = e^{+2 pi i j r / (NS RS)})
@@ -1580,7 +1581,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
         constexpr int KP2 = C::KPT / 2;
         const double2 *ph = reinterpret_cast<const double2 *>(cx.ring.ph(seq));
         const int kb = l * C::KPT;
-        if (kb < k0) {  // chunk layout [m][c][kk]; degrees >= k0 of the chunk are zero-padded (alow padded too)
+        // stage layout: KPT / 2 consecutive 2-degree chunks [hh][m][c][2] (one bin's rows 32 B apart in every chunk: the
+        // broadcast LDS.128s of a warp's 8 bins stay 2 wavefronts; [m][c][4] measured 4); degrees >= k0 are zero-padded
+        if (kb < k0) {
           double al[C::KPT];
 #pragma unroll
           for (int kk = 0; kk < C::KPT; ++kk) al[kk] = cx.alow[(kb + kk) * LG + line];
@@ -1591,7 +1594,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fwd_axis_kernel(AxisDev ax, co
             for (int c = 0; c < MAXR; ++c)
 #pragma unroll
               for (int hh = 0; hh < KP2; ++hh) {
-                const double2 pp = ph[(m[q] * MAXR + c) * KP2 + hh];
+                const double2 pp = ph[(hh * NBINS + m[q]) * MAXR + c];
                 y[q][c] = fma(pp.x, al[2 * hh], fma(pp.y, al[2 * hh + 1], y[q][c]));
               }
           }
@@ -2015,7 +2018,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) inv_axis_kernel(AxisDev ax, co
               if (!mir && kb < k0) {
 #pragma unroll
                 for (int hh = 0; hh < C::KPT / 2; ++hh) {
-                  const double2 pp = ph[(m[r] * MAXR + c) * (C::KPT / 2) + hh];
+                  const double2 pp = ph[(hh * NBINS + m[r]) * MAXR + c];
                   pv[2 * hh] = fma(pp.x, yv, pv[2 * hh]);
                   pv[2 * hh + 1] = fma(pp.y, yv, pv[2 * hh + 1]);
                 }

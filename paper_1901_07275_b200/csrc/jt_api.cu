@@ -348,7 +348,7 @@ jt_status upload_axis(jt_plan_s *p, int axis, bool pair = false) {
         }
       for (int k = 0; k < k0; ++k) {
         phivb[((size_t)k * MAXR + c) * nbins + m] = h.phiv[(size_t)j * k0 + k];
-        phivc[(((size_t)(k / KPT) * nbins + m) * MAXR + c) * KPT + (k % KPT)] = h.phiv[(size_t)j * k0 + k];
+        phivc[(((size_t)(k / 2) * nbins + m) * MAXR + c) * 2 + (k % 2)] = h.phiv[(size_t)j * k0 + k];  // 2-degree chunks
       }
     }
   }
