@@ -45,7 +45,11 @@ def single_gpu_cases():
              ((256, 256), (0.1, -0.25), (-0.4, 0.35)), ((33, 7), (0.0, 0.5), (0.0, -0.5)),
              ((17, 2048), (-0.2, 0.7), (0.1, 0.3)), ((64, 48, 40), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)),
              ((5, 130, 9), (0.25, 0.25, 0.25), (-0.25, -0.25, -0.25)), ((128, 96), (0.25, -0.3), (-0.1, 0.4)),
-             ((64, 64, 64), (0.1, 0.2, 0.3), (-0.1, -0.2, -0.3)), ((2000, 3), (0.1, 0.2), (0.3, -0.4))]
+             ((64, 64, 64), (0.1, 0.2, 0.3), (-0.1, -0.2, -0.3)), ((2000, 3), (0.1, 0.2), (0.3, -0.4)),
+             # launches of >= 2400 lines on FFT lengths 256 / 512 / 4096: the paired kernels (Cfg::PAIR), forward and
+             # inverse, incl. n below the FFT length; the host pipelines mix paired and unpaired chunk launches
+             ((2410, 256), (0.35, -0.2), (0.1, 0.3)), ((300, 2403), (0.3, -0.2), (0.2, 0.4)),
+             ((4096, 2401), (0.45, 0.25), (-0.45, -0.3))]
     for shape, a, b in cases:
         p = jt.Plan(shape, a, b, 1e-12)
         x = si.gaussian(shape, seed=7)
