@@ -221,7 +221,7 @@ jt_status jt_destroy(jt_plan_t p);
 /* ---- introspection (host; valid for host-only plans too) ---- */
 
 /* Rank r of axis `axis`'s factorisation (eq:approxA: Algorithm 1's complex factors).  It is the
- * number of complex FFTs per line of the unpaired kernels; uniform axes of FFT length 256 / 512 / 4096 also carry a
+ * number of complex FFTs per line of the unpaired kernels; uniform axes of FFT length 256 / 512 / 2048 / 4096 also carry a
  * second factor set with REAL v_l (two terms per complex FFT, about r/2 FFTs per line), which the library uses by
  * itself for launches of >= 2400 lines (DESIGN.md §6 and reading R26; jt_debug_pair_factors in jt_debug.h shows it;
  * JT_PAIR=0 in the environment at plan time disables it).  Results agree to the plan's eps either way. */

@@ -19,7 +19,7 @@ jt_status jt_debug_modified_pq(double a, double b, int64_t nt, const double *t, 
                                double *q_out);
 
 /* jt_debug_pair_factors: the plan's SECOND factor set of axis `axis`, used by its forward passes where the axis has
- * one (uniform axes of FFT length 512; DESIGN.md §6 "Two real rank terms per FFT"; the method is eq:oneJ,
+ * one (uniform axes of FFT length 256 / 512 / 2048 / 4096; DESIGN.md §6 "Two real rank terms per FFT"; the method is eq:oneJ,
  * PAPER.md:610, with a factorisation of eq:approxA whose v'_l are REAL, so two terms share one complex FFT):
  *   *r      number of FFTs (pairs) per line, 0 if the axis has no paired set (then nothing else is written)
  *   *rreal  number of real rank terms (2 r or 2 r - 1)

@@ -402,7 +402,7 @@ struct Cfg {
   }
   static_assert(GT % 32 == 0, "group must be whole warps");
   static_assert(!PAIR || INV || (MAXR == 2 && Pass<N, R, NSL>::B % 2 == 0 && Pass<N, R, NSL>::B * TPL == N / RSL &&
-                                 NSL > 1 && !VTM_PRE && !SUB && !URING_WANT),
+                                 NSL > 1 && !VTM_PRE && !SUB),
                 "PAIR forward: an even number of last-pass butterflies per thread");
   static_assert(!PAIR || !INV || (MAXR == 2 && Pass<N, R, 1>::B == 1 && Pass<N, R, 1>::RS == R && PRIV && !SUB),
                 "PAIR inverse: one radix-R first-pass butterfly per thread (positions vt + r TPL)");

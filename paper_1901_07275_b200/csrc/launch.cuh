@@ -375,8 +375,9 @@ jt_status launch_nm(LaunchState &st, bool inverse, const jtk::AxisDev &ax, const
 
 // FFT lengths with Cfg::PAIR forward kernels (the last Stockham pass must hold an even number of butterflies per
 // thread, so that a thread owns bin m and its conjugate mirror N - 1 - m): 512 = 32 x 16 (2 butterflies), 4096 =
-// 32 x 32 x 4 (8), and 256 as 32 x 8 (4; the unpaired N = 256 kernels are radix 16 = 16 x 16, one butterfly)
-constexpr bool pair_length(int64_t N) { return JT_PAIR && (N == 512 || N == 256 || N == 4096); }
+// 32 x 32 x 4 (8), 2048 = 16 x 16 x 8 (2), and 256 as 32 x 8 (4; the unpaired N = 256 kernels are radix 16 = 16 x 16,
+// one butterfly)
+constexpr bool pair_length(int64_t N) { return JT_PAIR && (N == 512 || N == 256 || N == 4096 || (JT_PAIR_2048 && N == 2048)); }
 constexpr int pair_radix(int64_t N) { return N == 256 ? 32 : radix_of(N, 2); }
 
 template <int N>

@@ -45,9 +45,13 @@
                       // 256^3 2.00 -> 2.03 ms, 128^3 -0.8 %)
 #endif
 #ifndef JT_PAIR
-#define JT_PAIR 1  // forward passes: two REAL rank terms per complex FFT (Cfg::PAIR kernels, N = 512; the plan's
+#define JT_PAIR 1  // forward passes: two REAL rank terms per complex FFT (Cfg::PAIR kernels, N = 256 / 512 / 2048 / 4096; the plan's
                    // second, real-row-space factor set: 9 FFTs instead of 16 per line at 512^3).  JT_PAIR=0 in the
                    // environment turns it off at plan time (A/B)
+#endif
+#ifndef JT_PAIR_2048
+#define JT_PAIR_2048 1  // ... also FFT length 2048 (16 x 16 x 8; its forward then reads u~ from L2 unless the doubled
+                        // u-ring stage still fits)
 #endif
 #ifndef JT_PAIR_INV
 #define JT_PAIR_INV 1  // ... also the inverse / transpose passes (the transposed paired operator)

@@ -16,7 +16,7 @@ if torch.cuda.is_available():
 
 TOL = 1e-10
 MIN_LINES = 2400  # csrc/tuning.h JT_PAIR_MIN_LINES
-PAIR_N = (256, 512, 4096)  # FFT lengths with paired kernels (csrc/launch.cuh pair_length)
+PAIR_N = (256, 512, 2048, 4096)  # FFT lengths with paired kernels (csrc/launch.cuh pair_length)
 
 
 def fft_length(n):
@@ -39,7 +39,7 @@ def fwd(p, x):
     return yd.cpu().numpy()
 
 
-# shapes whose axes of FFT length 256 / 512 / 4096 are transformed in launches of >= MIN_LINES lines (paired kernels),
+# shapes whose axes of FFT length 256 / 512 / 2048 / 4096 are transformed in launches of >= MIN_LINES lines (paired kernels),
 # with ragged line counts (not multiples of the CTA's line tile), every axis position, other axis lengths mixed in, and
 # axis lengths below their FFT length (n = 2403 -> N = 4096, 200 -> 256, 300 -> 512: zero-padded v, sparser bins)
 CASES = [((512, 2403), (0.25, 0.1), (-0.25, -0.3)),
@@ -49,7 +49,9 @@ CASES = [((512, 2403), (0.25, 0.1), (-0.25, -0.3)),
          ((61, 256, 41), (0.2, -0.4, 0.35), (-0.2, 0.3, 0.1)),
          ((4096, 2401), (0.45, 0.25), (-0.45, -0.3)),
          ((2405, 4096), (0.1, 0.0), (-0.1, 0.0)),
-         ((200, 300, 41), (0.3, -0.2, 0.1), (0.2, 0.4, -0.3))]
+         ((200, 300, 41), (0.3, -0.2, 0.1), (0.2, 0.4, -0.3)),
+         ((2048, 2405), (-0.3, 0.2), (0.6, 0.1)),
+         ((2409, 2000), (0.15, 0.4), (-0.35, -0.4))]
 
 
 @pytest.mark.parametrize("shape,a,b", CASES)

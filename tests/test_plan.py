@@ -311,11 +311,21 @@ def test_paired_factors_vs_oracle(a, b):
 
 
 def test_pair_env_off(monkeypatch):
+    """JT_PAIR=0 at plan time: no paired set; FFT lengths without paired kernels (1024: one last-pass butterfly per
+    thread) never have one; 256 / 2048 / 4096 do (csrc/launch.cuh pair_length)."""
     monkeypatch.setenv("JT_PAIR", "0")
     p = jt.Plan(512, 0.25, -0.25, 1e-12, device=-2)
     assert jt.jt_debug_pair_factors(p.handle, 0) is None
     p.close()
-    q = jt.Plan(256, 0.25, -0.25, 1e-12, device=-2)  # no paired kernels at this FFT length
     monkeypatch.delenv("JT_PAIR")
+    q = jt.Plan(1024, 0.25, -0.3, 1e-12, device=-2)
     assert jt.jt_debug_pair_factors(q.handle, 0) is None
     q.close()
+    for n in (256, 200, 2048):
+        q = jt.Plan(n, 0.1, -0.2, 1e-12, device=-2)
+        got = jt.jt_debug_pair_factors(q.handle, 0)
+        assert got is not None and got[1].shape[0] < q.rank()
+        x = si.gaussian((n,), seed=n)
+        ref = oracle.phi(n, 0.1, -0.2) @ x
+        assert np.linalg.norm(pair_apply_np(q, x) - ref) <= 1e-11 * np.linalg.norm(ref)
+        q.close()

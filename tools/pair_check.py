@@ -38,8 +38,10 @@ def child():
                                                      for i in range(len(shape))]}
         p.close()
     # timing: the BASELINE configs' forwards, sampled oracle check of the full-size outputs
-    for name in ("cfg2_2d_256", "cfg4_3d_256", "cfg3_2d_4096", "cfg5_3d_512"):
-        c = si.CONFIGS[name]
+    for name in ("cfg2_2d_256", "cfg4_3d_256", "cfg3_2d_4096", "cfg5_3d_512", "grid_2048x2048", "grid_2048x2048x8"):
+        c = si.CONFIGS[name] if name in si.CONFIGS else {
+            "n": tuple(int(v) for v in name[5:].split("x")), "eps": 1e-12,
+            "a": (0.25, -0.3, 0.1)[:len(name[5:].split("x"))], "b": (-0.25, 0.2, 0.3)[:len(name[5:].split("x"))]}
         shape = tuple(c["n"])
         p = jt.Plan(shape, c["a"], c["b"], c["eps"])
         x = si.gaussian(shape, seed=0)
