@@ -632,13 +632,19 @@ jt_status build_axis_host(AxisHost &ax, int64_t n, double a, double b, double ep
     // conjugate mirror N - 1 - m pair up uniformly; at most 2 rows per bin (no spreading: the caller falls back)
     ax.bins.assign(n, 0);
     ax.bstart.assign(ax.N / 2 + 2, 0);
+    // (where the nodes drift across a bin boundary -- a + b far from 0 -- a bin would take 3: the node moves to the
+    // next bin, at most one bin right of its own, bins staying non-decreasing in j; the factorisation absorbs the
+    // larger residual as in reading R21; failing that the caller keeps the unpaired set)
+    int32_t prev = 0;
     for (int64_t j = 0; j < n; ++j) {
-      const int32_t m = (int32_t)floorl(t[j] * (ld)ax.N / (2 * PI_L));
-      if (m < 0 || m >= ax.N / 2 || (j > 0 && m < ax.bins[j - 1]) || ax.bstart[m + 1] >= 2) {
+      const int32_t m0 = (int32_t)floorl(t[j] * (ld)ax.N / (2 * PI_L));
+      int32_t m = std::max(m0, prev);
+      while (m >= 0 && m < ax.N / 2 && ax.bstart[m + 1] >= 2) ++m;
+      if (m0 < 0 || m >= ax.N / 2 || m - m0 > 1) {
         err = "pair: more than 2 nodes in a half-integer FFT bin";
         return JT_ERR_NUMERIC;
       }
-      ax.bins[j] = m;
+      ax.bins[j] = prev = m;
       ax.bstart[m + 1]++;
     }
   } else

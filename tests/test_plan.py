@@ -329,3 +329,23 @@ def test_pair_env_off(monkeypatch):
         ref = oracle.phi(n, 0.1, -0.2) @ x
         assert np.linalg.norm(pair_apply_np(q, x) - ref) <= 1e-11 * np.linalg.norm(ref)
         q.close()
+
+
+@pytest.mark.parametrize("n,a,b", [(512, -0.3, 0.6), (2048, -0.3, 0.6), (512, 0.7, 0.6)])
+def test_paired_bins_spill(n, a, b):
+    """(a, b) whose nodes drift across a half-integer bin boundary (a + b far from 0): a third node of a bin moves to
+    the next bin (plan.cpp, pair bins); the paired set still reproduces the oracle's product, or the plan falls back
+    to the unpaired set (None)."""
+    p = jt.Plan(n, a, b, 1e-12, device=-2)
+    got = jt.jt_debug_pair_factors(p.handle, 0)
+    if got is not None:
+        u, v, phiv, bins, rreal = got
+        t, _ = p.nodes()
+        d = bins - np.floor(t * n / (2 * np.pi)).astype(np.int32)
+        assert d.min() >= 0 and d.max() <= 1 and np.all(np.diff(bins) >= 0)
+        assert np.bincount(bins, minlength=n // 2).max() <= 2 and bins.max() < n // 2
+        assert v.shape[0] < p.rank()
+        x = si.gaussian((n,), seed=n + 1)
+        ref = oracle.phi(n, a, b) @ x
+        assert np.linalg.norm(pair_apply_np(p, x) - ref) <= 1e-11 * np.linalg.norm(ref)
+    p.close()
